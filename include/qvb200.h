@@ -1,0 +1,147 @@
+/*
+ * qvb200.h — C ABI of the B200 state-vector executor (libqvb200.so).
+ *
+ * This is the drop-in boundary for the reference's accelerator plugin
+ * surface.  The reference binds no native code (its "kernels" are numba
+ * functions), so each entry point below names the Python interface it
+ * replaces; `INTEGRATION.md` shows the ctypes stub a maintainer of the
+ * reference would add to `qvirt/backend.py`.
+ *
+ *   qv_create / qv_destroy   <- one `StatevectorBackend()` instance per
+ *                               worker thread (reference pkg/src/qvirt/backend.py:283-295,
+ *                               created by `backend_factory()` in pool.py:113-114).
+ *   qv_execute               <- `StatevectorBackend.execute(buffer, circuits, config)`
+ *                               in expectation mode (backend.py:293-313):
+ *                               allocate (:151-157) -> run_gates (:182-185, kernels.py:18-70)
+ *                               -> expectation (:188-213, kernels.py:73-87)
+ *                               or born_distribution (:216-231, kernels.py:90-94).
+ *   qv_last_error*           <- `ExecutionError(circuit_name, message)` (backend.py:130-135):
+ *                               the failing circuit index lets the caller raise with the name.
+ *
+ * Conventions (same as the reference, kernels.py:3-7): qubit 0 is the MOST
+ * significant bit of an amplitude index; qubit q flips index bit n-1-q.  All
+ * pointers are host pointers owned by the caller for the duration of the call;
+ * no CUDA or torch types cross this boundary.  Calls never throw; they return
+ * a status code.  Calls on one handle are serialised by the handle; distinct
+ * handles may be driven from distinct threads (ctypes releases the GIL).
+ */
+#ifndef QVB200_H
+#define QVB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes -------------------------------------------------------- */
+#define QV_OK 0
+#define QV_ERR_ARGUMENT 1   /* bad arguments / malformed batch (reference: ValueError)  */
+#define QV_ERR_CIRCUIT 2    /* a circuit failed; see qv_last_error_circuit (ExecutionError) */
+#define QV_ERR_CUDA 3       /* CUDA runtime failure (out of memory, launch error, no device) */
+#define QV_ERR_INTERNAL 4
+
+/* ---- gate kinds (reference circuits.py:27-33 GateKind; RX/CZ are extensions) */
+#define QV_GATE_H 0
+#define QV_GATE_X 1
+#define QV_GATE_CNOT 2      /* q0 = control, q1 = target */
+#define QV_GATE_RY 3
+#define QV_GATE_RZ 4
+#define QV_GATE_MEASURE_ALL 5 /* no-op in exact mode (backend.py:160-179) */
+#define QV_GATE_RX 6        /* extension: [[c,-is],[-is,c]]                  */
+#define QV_GATE_CZ 7        /* extension: diag(1,1,1,-1) on (q0,q1)           */
+
+/* ---- amplitude precision -------------------------------------------------- */
+#define QV_COMPLEX128 0     /* the reference's only precision (backend.py:155) */
+#define QV_COMPLEX64 1      /* complex64 states, FP64 reductions                */
+
+/* ---- result kinds --------------------------------------------------------- */
+#define QV_OUT_PAULI 0      /* per circuit, per term: <P> (coefficient-free, kernels.py:73-87)  */
+#define QV_OUT_SUPPORT 1    /* per circuit: normalised p on `support` + the norm (backend.py:216-223) */
+#define QV_OUT_FULL 2       /* per circuit: all 2^n normalised probabilities (n <= 24)          */
+#define QV_OUT_JS 3         /* per circuit: JS(target || p) via the support+remainder identity  */
+                            /* (ddcl.py:37-61 over born_distribution)                            */
+
+typedef struct qv_engine* qv_handle;
+
+/* A batch of bound circuits on one register width.
+ * uniform = 1: every circuit has the same gate list (kinds/q0/q1 of length n_gates)
+ *              and `angles` is an [n_circuits][n_gates] row-major table
+ *              (the structure of a parameter-shift batch, gradients.py:33-46).
+ * uniform = 0: circuit c owns gates [gate_offsets[c], gate_offsets[c+1]) of
+ *              kinds/q0/q1/angles.
+ * Angles of non-rotation gates are ignored.  q1 is ignored for 1-qubit gates. */
+typedef struct qv_circuits {
+    int32_t n_qubits;
+    int32_t n_circuits;
+    int32_t uniform;
+    int32_t reserved;
+    int64_t n_gates;               /* uniform = 1 */
+    const int64_t* gate_offsets;   /* uniform = 0: n_circuits + 1 entries */
+    const uint8_t* kinds;
+    const int32_t* q0;
+    const int32_t* q1;
+    const double* angles;
+} qv_circuits;
+
+/* What to return for each circuit. */
+typedef struct qv_results {
+    int32_t kind;                  /* QV_OUT_* */
+    int32_t reserved;
+    /* QV_OUT_PAULI: circuit c owns terms [term_offsets[c], term_offsets[c+1]);
+     * a term is a Pauli product given by qubit-bit masks (bit n-1-q for qubit q),
+     * exactly the (xmask, ymask, zmask) of backend.py:198-213.                 */
+    const int64_t* term_offsets;
+    const uint64_t* xmask;
+    const uint64_t* ymask;
+    const uint64_t* zmask;
+    /* QV_OUT_SUPPORT / QV_OUT_JS: one support shared by the whole batch,
+     * sorted ascending, unique amplitude indices; `target` (JS only) holds the
+     * target probability of each support index.                                */
+    int64_t support_count;
+    const uint64_t* support;
+    const double* target;
+} qv_results;
+
+/* Output sizes (doubles) written to `out`:
+ *   PAULI   : term_offsets[n_circuits]                     (term t of circuit c at term_offsets[c]+t)
+ *   SUPPORT : n_circuits * (support_count + 1)             (row: p_0..p_{S-1}, norm)
+ *   FULL    : n_circuits * 2^n_qubits
+ *   JS      : n_circuits                                                              */
+int64_t qv_output_size(const qv_circuits* circuits, const qv_results* results);
+
+/* Create an executor bound to CUDA device `device`.  `memory_budget_bytes`
+ * caps the device memory this handle keeps for state vectors (0 = 85% of the
+ * device memory that is free at creation). */
+int qv_create(int device, int precision, uint64_t memory_budget_bytes, qv_handle* out);
+int qv_destroy(qv_handle handle);
+
+/* Execute a batch; blocks until `out` holds the results. */
+int qv_execute(qv_handle handle, const qv_circuits* circuits, const qv_results* results,
+               double* out, int64_t out_len);
+
+/* Last error of this handle (empty string if none) and the index of the
+ * circuit it belongs to (-1 if it is not specific to one circuit). */
+const char* qv_last_error(qv_handle handle);
+int64_t qv_last_error_circuit(qv_handle handle);
+
+/* Execution statistics of the last qv_execute call on this handle:
+ * [0] kernel launches, [1] full state sweeps executed (passes x states),
+ * [2] sweeps a schedule without prefix sharing would run, [3] unique states simulated,
+ * [4] algorithmic HBM bytes moved by pass kernels, [5] device ms of pass kernels
+ * (CUDA events on the executor stream), [6] passes per circuit, [7] tile bits k,
+ * [8] total device ms of the call. */
+int qv_last_stats(qv_handle handle, double* stats, int32_t n_stats);
+
+/* Library version string, e.g. "qvb200 0.1 sm_100a". */
+const char* qv_version(void);
+
+/* Number of visible CUDA devices (0 if none / no driver).  The virtual-QPU
+ * pool maps vQPU b to device b mod qv_device_count() (pool.py:88-138). */
+int qv_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QVB200_H */

@@ -1,0 +1,333 @@
+// plan.cpp — see plan.hpp.
+//
+// Gate semantics restated from the reference kernels (pkg/src/qvirt/kernels.py):
+//   H  :18-27   (a0+a1, a0-a1) * 1/sqrt(2)
+//   X  :30-37   swap
+//   RY :40-50   [[c,-s],[s,c]], c = cos(theta/2), s = sin(theta/2)
+//   RZ :53-59   diag(exp(-i theta/2), exp(+i theta/2))
+//   CNOT :62-70 swap a[i], a[i|t] where the control bit is set
+// RX / CZ are extensions (not in the reference gate set, circuits.py:27-33):
+//   RX = [[c,-is],[-is,c]];  CZ(a,b) = H_b CNOT(a,b) H_b.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <stdexcept>
+
+namespace qvb {
+
+namespace {
+
+using cd = std::complex<double>;
+
+inline int popcount64(uint64_t v) { return __builtin_popcountll(v); }
+
+uint64_t op_mask(const FusedOp& op) {
+    uint64_t m = 1ull << op.b0;
+    if (op.cnot) m |= 1ull << op.b1;
+    return m;
+}
+
+int coalesce_bits(int precision) { return precision == 0 ? 3 : 4; }  // 2^c amps = 128 B
+int bank_bits(int precision) { return precision == 0 ? 3 : 4; }      // 16 B / 8 B words per 128 B row
+
+std::vector<FusedOp> fuse(const Topology& t) {
+    std::vector<FusedOp> ops;
+    std::vector<int> open(kMaxQubits + 1, -1);
+    const int n = t.n;
+    auto add_1q = [&](int b, int32_t ref) {
+        if (open[b] >= 0) {
+            ops[open[b]].gates.push_back(ref);
+        } else {
+            open[b] = (int)ops.size();
+            FusedOp op;
+            op.b0 = b;
+            op.gates.push_back(ref);
+            ops.push_back(std::move(op));
+        }
+    };
+    auto add_cnot = [&](int c, int tb) {
+        open[c] = -1;
+        open[tb] = -1;
+        FusedOp op;
+        op.cnot = true;
+        op.b0 = c;
+        op.b1 = tb;
+        ops.push_back(std::move(op));
+    };
+    for (size_t g = 0; g < t.kind.size(); ++g) {
+        const uint8_t k = t.kind[g];
+        if (k == G_MEASURE) continue;
+        if (k == G_CNOT) {
+            add_cnot(n - 1 - t.q0[g], n - 1 - t.q1[g]);
+        } else if (k == G_CZ) {
+            const int a = n - 1 - t.q0[g], b = n - 1 - t.q1[g];
+            add_1q(b, -1);
+            add_cnot(a, b);
+            add_1q(b, -1);
+        } else {
+            add_1q(n - 1 - t.q0[g], (int32_t)g);
+        }
+    }
+    return ops;
+}
+
+// Greedy pass selection.  Each pass owns k index bits (always including the
+// low `c` bits so every tile row is a contiguous 128 B run); it applies, in
+// program order, every op whose bits lie in the pass and that does not depend
+// on an op left for a later pass.  Two-qubit ops claim bits first (they are
+// what forces new passes), one-qubit ops fill the remaining capacity.
+std::vector<PassPlan> select_passes(int n, int k, int c, const std::vector<FusedOp>& ops) {
+    std::vector<PassPlan> passes;
+    std::vector<int> rem(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) rem[i] = (int)i;
+    const uint64_t low = (1ull << c) - 1;
+    while (!rem.empty()) {
+        uint64_t S = low;
+        uint64_t blocked = 0;
+        for (int i : rem) {
+            const uint64_t bits = op_mask(ops[i]);
+            if (bits & blocked) { blocked |= bits; continue; }
+            if (!ops[i].cnot || !(bits & ~S)) continue;
+            if (popcount64(S | bits) <= k) S |= bits;
+            else blocked |= bits;
+        }
+        blocked = 0;
+        for (int i : rem) {
+            const uint64_t bits = op_mask(ops[i]);
+            if (bits & blocked) { blocked |= bits; continue; }
+            if (!(bits & ~S)) continue;
+            if (!ops[i].cnot && popcount64(S | bits) <= k) { S |= bits; continue; }
+            blocked |= bits;
+        }
+        for (int b = 0; b < n && popcount64(S) < k; ++b) S |= 1ull << b;
+        PassPlan pp;
+        std::vector<int> left;
+        blocked = 0;
+        for (int i : rem) {
+            const uint64_t bits = op_mask(ops[i]);
+            if ((bits & blocked) || (bits & ~S)) { blocked |= bits; left.push_back(i); continue; }
+            pp.ops.push_back(i);
+        }
+        if (pp.ops.empty()) throw std::runtime_error("pass planner made no progress");
+        for (int b = 0; b < n; ++b)
+            if ((S >> b) & 1) pp.S.push_back(b);
+        passes.push_back(std::move(pp));
+        rem.swap(left);
+    }
+    if (passes.empty()) {  // empty circuit: one pass that applies nothing
+        PassPlan pp;
+        for (int b = 0; b < k; ++b) pp.S.push_back(b);
+        passes.push_back(pp);
+    }
+    return passes;
+}
+
+struct GroupBuilder {
+    int k, beta;
+    uint16_t col[16];      // logical-bit -> slot column (before swizzle): the map Q
+    std::vector<std::pair<int, int>> open;  // (logical bit, pass-local matrix index)
+
+    uint16_t swz(uint32_t v) const {   // bank swizzle, GF(2)-linear
+        uint32_t r = v;
+        for (int j = beta; j < k; ++j)
+            if ((v >> j) & 1u) r ^= 1u << (j % beta);
+        return (uint16_t)r;
+    }
+    uint16_t phys(int b) const { return swz(col[b]); }
+
+    void close(std::vector<GroupDesc>& out) {
+        if (open.empty()) return;
+        GroupDesc g;
+        std::memset(&g, 0, sizeof(g));
+        int reg[kRegBits];
+        uint32_t used = 0;
+        int nr = 0;
+        for (auto& pr : open) { reg[nr] = pr.first; g.mat[nr] = (int16_t)pr.second; used |= 1u << pr.first; ++nr; }
+        for (int b = k - 1; b >= 0 && nr < kRegBits; --b)
+            if (!((used >> b) & 1u)) { reg[nr] = b; g.mat[nr] = -1; used |= 1u << b; ++nr; }
+        // complement bits -> thread bits; the first `beta` of them index the
+        // lanes of one shared-memory wavefront, pick them with independent
+        // bank projections so those accesses are conflict-free
+        std::vector<int> comp;
+        for (int b = 0; b < k; ++b)
+            if (!((used >> b) & 1u)) comp.push_back(b);
+        std::vector<int> order;
+        std::vector<bool> taken(comp.size(), false);
+        const uint32_t bmask = (1u << beta) - 1;
+        uint32_t span = 1u;   // set of bank indices spanned so far ({0})
+        for (size_t i = 0; i < comp.size() && (int)order.size() < beta; ++i) {
+            const uint32_t v = phys(comp[i]) & bmask;
+            if ((span >> v) & 1u) continue;   // dependent on the lanes chosen so far
+            uint32_t grown = span;
+            for (uint32_t e = 0; e <= bmask; ++e)
+                if ((span >> e) & 1u) grown |= 1u << (e ^ v);
+            span = grown;
+            order.push_back(comp[i]);
+            taken[i] = true;
+        }
+        for (size_t i = 0; i < comp.size(); ++i)
+            if (!taken[i]) order.push_back(comp[i]);
+        for (int j = 0; j < kGroupAmps; ++j) {
+            uint16_t s = 0;
+            for (int r = 0; r < kRegBits; ++r)
+                if ((j >> r) & 1) s ^= phys(reg[r]);
+            g.combo[j] = s;
+        }
+        for (size_t m = 0; m < order.size(); ++m) g.tcol[m] = phys(order[m]);
+        out.push_back(g);
+        open.clear();
+    }
+};
+
+}  // namespace
+
+std::string Topology::key() const {
+    std::string s;
+    s.reserve(8 + kind.size() * 9);
+    s.append(reinterpret_cast<const char*>(&n), sizeof(n));
+    for (size_t g = 0; g < kind.size(); ++g) {
+        s.push_back((char)kind[g]);
+        s.append(reinterpret_cast<const char*>(&q0[g]), sizeof(int32_t));
+        const int32_t b = is_two_qubit(kind[g]) ? q1[g] : -1;
+        s.append(reinterpret_cast<const char*>(&b), sizeof(int32_t));
+    }
+    return s;
+}
+
+int tile_bits_for(int n, int precision) {
+    const int kmax = precision == 0 ? 12 : 13;
+    if (n <= kmax) return std::max(n, kRegBits);
+    return kmax;
+}
+
+Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
+    Plan plan;
+    plan.n = topo.n;
+    plan.precision = precision;
+    plan.k = tile_bits_for(topo.n, precision);
+    if (max_tile_bits > 0) {
+        if (max_tile_bits < coalesce_bits(precision) + 2 || max_tile_bits > kMaxTileBits)
+            throw std::runtime_error("tile bits out of range");
+        plan.k = topo.n <= max_tile_bits ? std::max(topo.n, kRegBits) : max_tile_bits;
+    }
+    plan.single_tile = topo.n <= plan.k;
+    plan.ops = fuse(topo);
+    const int n = topo.n, k = plan.k;
+    const int beta = bank_bits(precision);
+    if (plan.single_tile) {
+        PassPlan pp;
+        for (int b = 0; b < k; ++b) pp.S.push_back(b);
+        for (size_t i = 0; i < plan.ops.size(); ++i) pp.ops.push_back((int)i);
+        plan.passes.push_back(std::move(pp));
+    } else {
+        plan.passes = select_passes(n, k, coalesce_bits(precision), plan.ops);
+    }
+    for (auto& pp : plan.passes) {
+        PassDesc d;
+        std::memset(&d, 0, sizeof(d));
+        d.k = k;
+        d.n_outer = plan.single_tile ? 0 : n - k;
+        int logical_of[64];
+        for (int b = 0; b < 64; ++b) logical_of[b] = -1;
+        for (int j = 0; j < k; ++j) { d.sbits[j] = (uint8_t)pp.S[j]; logical_of[pp.S[j]] = j; }
+        if (!plan.single_tile) {
+            int o = 0;
+            for (int b = 0; b < n; ++b)
+                if (logical_of[b] < 0) d.obits[o++] = (uint8_t)b;
+        }
+        GroupBuilder gb;
+        gb.k = k;
+        gb.beta = beta;
+        for (int j = 0; j < 16; ++j) gb.col[j] = (uint16_t)(j < k ? 1u << j : 0);
+        for (int j = 0; j < k; ++j) d.swz[j] = gb.phys(j);
+        d.g0 = (int)plan.groups.size();
+        d.m0 = (int)plan.mat_op.size();
+        int local_mats = 0;
+        for (int oi : pp.ops) {
+            const FusedOp& op = plan.ops[oi];
+            if (!op.cnot) {
+                const int lb = logical_of[op.b0];
+                bool clash = false;
+                for (auto& pr : gb.open) clash |= pr.first == lb;
+                if (clash || (int)gb.open.size() == kRegBits) gb.close(plan.groups);
+                gb.open.push_back({lb, local_mats++});
+                plan.mat_op.push_back(oi);
+            } else {
+                const int lc = logical_of[op.b0], lt = logical_of[op.b1];
+                bool clash = false;
+                for (auto& pr : gb.open) clash |= pr.first == lc || pr.first == lt;
+                if (clash) gb.close(plan.groups);
+                gb.col[lc] ^= gb.col[lt];   // Q <- Q o CNOT
+            }
+        }
+        gb.close(plan.groups);
+        d.ng = (int)plan.groups.size() - d.g0;
+        d.nm = local_mats;
+        for (int j = 0; j < k; ++j) d.fin[j] = gb.phys(j);
+        for (int it = 0; it < 16; ++it) {
+            const uint32_t idx = (uint32_t)it << (k - kRegBits);
+            d.swz_hi[it] = (uint16_t)apply_cols(d.swz, k, idx);
+            d.fin_hi[it] = (uint16_t)apply_cols(d.fin, k, idx);
+            uint64_t g = 0;
+            for (int i = 0; i < kRegBits; ++i)
+                if ((it >> i) & 1) g |= 1ull << d.sbits[k - kRegBits + i];
+            d.g_hi[it] = g;
+        }
+        pp.n_groups = d.ng;
+        pp.n_mats = d.nm;
+        plan.pdesc.push_back(d);
+    }
+    return plan;
+}
+
+namespace {
+struct M2 { cd a, b, c, d; };  // [[a,b],[c,d]]
+M2 mul(const M2& x, const M2& y) {  // x * y
+    return {x.a * y.a + x.b * y.c, x.a * y.b + x.b * y.d, x.c * y.a + x.d * y.c, x.c * y.b + x.d * y.d};
+}
+M2 gate_matrix(const Topology& t, int32_t ref, const double* angles) {
+    const double inv = 1.0 / std::sqrt(2.0);
+    if (ref < 0) return {cd(inv, 0), cd(inv, 0), cd(inv, 0), cd(-inv, 0)};
+    const uint8_t k = t.kind[ref];
+    switch (k) {
+        case G_H: return {cd(inv, 0), cd(inv, 0), cd(inv, 0), cd(-inv, 0)};
+        case G_X: return {cd(0, 0), cd(1, 0), cd(1, 0), cd(0, 0)};
+        case G_RY: {
+            const double c = std::cos(angles[ref] / 2.0), s = std::sin(angles[ref] / 2.0);
+            return {cd(c, 0), cd(-s, 0), cd(s, 0), cd(c, 0)};
+        }
+        case G_RZ: {
+            const double c = std::cos(angles[ref] / 2.0), s = std::sin(angles[ref] / 2.0);
+            return {cd(c, -s), cd(0, 0), cd(0, 0), cd(c, s)};
+        }
+        case G_RX: {
+            const double c = std::cos(angles[ref] / 2.0), s = std::sin(angles[ref] / 2.0);
+            return {cd(c, 0), cd(0, -s), cd(0, -s), cd(c, 0)};
+        }
+        default: throw std::runtime_error("not a one-qubit gate");
+    }
+}
+}  // namespace
+
+void circuit_matrices(const Plan& plan, const Topology& topo, const double* angles, double* out) {
+    for (int s = 0; s < plan.n_slots(); ++s) {
+        const FusedOp& op = plan.ops[plan.mat_op[s]];
+        M2 m{cd(1, 0), cd(0, 0), cd(0, 0), cd(1, 0)};
+        bool first = true;
+        for (int32_t ref : op.gates) {
+            const M2 g = gate_matrix(topo, ref, angles);
+            m = first ? g : mul(g, m);
+            first = false;
+        }
+        double* o = out + (size_t)s * 8;
+        o[0] = m.a.real(); o[1] = m.a.imag();
+        o[2] = m.b.real(); o[3] = m.b.imag();
+        o[4] = m.c.real(); o[5] = m.c.imag();
+        o[6] = m.d.real(); o[7] = m.d.imag();
+    }
+}
+
+}  // namespace qvb

@@ -1,0 +1,121 @@
+// plan.hpp — circuit topology -> fused ops -> HBM passes -> register groups.
+//
+// A *topology* is a gate list without angles (kinds + qubits).  Everything in
+// a plan depends on the topology only, never on angles or on which other
+// circuits share a batch, so every circuit's arithmetic is a function of the
+// circuit alone: results are bitwise independent of how a batch is split
+// across virtual QPUs / GPUs (the reference's serial-equivalence law,
+// pkg/src/qvirt/pool.py:10-14).
+//
+// Index convention (reference kernels.py:3-7): qubit q <-> amplitude index
+// bit b = n-1-q.  Internally everything is expressed in bits.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace qvb {
+
+constexpr int kRegBits = 4;          // register bits per group: 16 amplitudes per thread
+constexpr int kGroupAmps = 1 << kRegBits;
+constexpr int kMaxTileBits = 13;     // 2^13 amplitudes (64 KiB at complex64, 128 KiB c128)
+constexpr int kMaxQubits = 40;
+
+enum GateKind : uint8_t { G_H = 0, G_X = 1, G_CNOT = 2, G_RY = 3, G_RZ = 4, G_MEASURE = 5, G_RX = 6, G_CZ = 7 };
+
+inline bool is_rotation(uint8_t k) { return k == G_RY || k == G_RZ || k == G_RX; }
+inline bool is_two_qubit(uint8_t k) { return k == G_CNOT || k == G_CZ; }
+
+struct Topology {
+    int n = 0;
+    std::vector<uint8_t> kind;
+    std::vector<int32_t> q0, q1;
+    std::string key() const;         // exact identity of the topology (n + gate list)
+};
+
+// A fused operation: a maximal run of 1-qubit gates on one bit (MAT1, the
+// matrix is the ordered product of its gates) or one CNOT.  `gates` holds
+// topology gate indices; -1 stands for a constant Hadamard (CZ lowering).
+struct FusedOp {
+    bool cnot = false;
+    int b0 = 0;       // MAT1: bit; CNOT: control bit
+    int b1 = -1;      // CNOT: target bit
+    std::vector<int32_t> gates;
+};
+
+// Device descriptor of one register group: a thread loads 16 amplitudes from
+// physical shared-memory slots base(tid) ^ combo[j], applies up to 4 2x2
+// matrices on register bits 0..3 and stores them back.
+struct alignas(16) GroupDesc {
+    uint16_t combo[16];
+    uint16_t tcol[10];   // physical column of thread bit m (tile bits - 4 of them)
+    int16_t mat[4];      // matrix index within the pass (-1 = identity)
+    uint16_t pad[2];
+};
+static_assert(sizeof(GroupDesc) == 64, "GroupDesc layout");
+
+// Device descriptor of one pass (one HBM sweep over every tile of a state).
+struct alignas(16) PassDesc {
+    int32_t k;           // tile bits (logical local bits 0..k-1)
+    int32_t n_outer;     // n - k outer (tile-index) bits
+    int32_t g0, ng;      // group range in the plan's group array
+    int32_t m0, nm;      // matrix slot range in a circuit's matrix table
+    int32_t pad0, pad1;
+    uint8_t sbits[16];   // logical local bit j -> global index bit
+    uint8_t obits[40];   // outer bit j -> global index bit
+    uint16_t swz[16];    // physical slot column of logical bit j at load time
+    uint16_t fin[16];    // physical slot column of logical bit j at store time
+    uint16_t swz_hi[16]; // physical slot of (it << (k-4)), it = 0..15, at load
+    uint16_t fin_hi[16]; // same at store
+    uint64_t g_hi[16];   // global offset of (it << (k-4))
+};
+
+struct PassPlan {
+    std::vector<int> S;      // global bits in the tile, ascending (size k)
+    std::vector<int> ops;    // fused-op indices applied, program order
+    int n_groups = 0;
+    int n_mats = 0;
+};
+
+struct Plan {
+    int n = 0;
+    int k = 0;               // tile bits
+    int precision = 0;       // 0 = complex128, 1 = complex64
+    bool single_tile = false;
+    std::vector<FusedOp> ops;
+    std::vector<int> mat_op;         // matrix slot -> fused op (slots ordered pass by pass)
+    std::vector<PassPlan> passes;
+    std::vector<PassDesc> pdesc;
+    std::vector<GroupDesc> groups;
+    int n_slots() const { return (int)mat_op.size(); }
+};
+
+// Tile bits used for a register of n qubits at a precision.
+int tile_bits_for(int n, int precision);
+
+// Build the full plan (fusion, pass selection, groups, descriptors).
+// `max_tile_bits` > 0 overrides the precision's tile size (tests use small
+// tiles to exercise the multi-tile planner on registers a CPU can check).
+Plan build_plan(const Topology& topo, int precision, int max_tile_bits = 0);
+
+// Fused 2x2 matrices of every slot for one circuit: out[slot*8 + 0..7] =
+// (m00.re, m00.im, m01.re, m01.im, m10.re, m10.im, m11.re, m11.im).
+// `angles` is indexed by topology gate index.
+void circuit_matrices(const Plan& plan, const Topology& topo, const double* angles, double* out);
+
+#ifdef __CUDACC__
+#define QV_HD __host__ __device__
+#else
+#define QV_HD
+#endif
+
+// Physical slot of a logical local index under a column map.
+QV_HD inline uint32_t apply_cols(const uint16_t* cols, int k, uint32_t idx) {
+    uint32_t r = 0;
+    for (int j = 0; j < k; ++j)
+        if ((idx >> j) & 1u) r ^= cols[j];
+    return r;
+}
+
+}  // namespace qvb

@@ -1,0 +1,118 @@
+// plancheck.cpp — TEST-ONLY library (libqvb200_plan.so).
+//
+// Interprets a plan exactly as pass_kernel does (tile staging through the
+// swizzled slot maps, register groups, CNOTs folded into the slot maps) but on
+// the host with std::complex<double>, so CPU tests can check the planner's
+// GF(2) bookkeeping against the oracle without a GPU.  The product library
+// (libqvb200.so) does not contain this code and never calls it.
+#include <complex>
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "plan.hpp"
+
+using namespace qvb;
+using cd = std::complex<double>;
+
+namespace {
+Topology make_topo(int n, int64_t ng, const uint8_t* kinds, const int32_t* q0, const int32_t* q1) {
+    Topology t;
+    t.n = n;
+    t.kind.assign(kinds, kinds + ng);
+    t.q0.assign(q0, q0 + ng);
+    t.q1.assign(q1, q1 + ng);
+    for (int64_t g = 0; g < ng; ++g)
+        if (!is_two_qubit(t.kind[g])) t.q1[g] = -1;
+    return t;
+}
+}  // namespace
+
+extern "C" {
+
+// Final state of one circuit after running its plan; out = 2 * 2^n doubles.
+// Returns the number of passes, or -1 on error.
+int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                 const double* angles, int precision, int max_tile_bits, double* out) {
+    try {
+        const Topology topo = make_topo(n, n_gates, kinds, q0, q1);
+        const Plan plan = build_plan(topo, precision, max_tile_bits);
+        std::vector<double> mats((size_t)plan.n_slots() * 8);
+        circuit_matrices(plan, topo, angles, mats.data());
+        const int k = plan.k, tb = k - kRegBits, nt = 1 << tb;
+        const size_t dim = (size_t)1 << std::max(n, k);
+        std::vector<cd> st(dim, cd(0, 0)), tile((size_t)1 << k);
+        st[0] = 1.0;
+        for (const PassDesc& pd : plan.pdesc) {
+            const int64_t ntiles = plan.single_tile ? 1 : (1ll << pd.n_outer);
+            for (int64_t x = 0; x < ntiles; ++x) {
+                uint64_t outer = 0;
+                for (int j = 0; j < pd.n_outer; ++j)
+                    if ((x >> j) & 1) outer |= 1ull << pd.obits[j];
+                for (int tid = 0; tid < nt; ++tid) {
+                    uint32_t ts = 0;
+                    uint64_t tg = 0;
+                    for (int j = 0; j < tb; ++j)
+                        if ((tid >> j) & 1) { ts ^= pd.swz[j]; tg |= 1ull << pd.sbits[j]; }
+                    for (int it = 0; it < 16; ++it) tile[ts ^ pd.swz_hi[it]] = st[outer | tg | pd.g_hi[it]];
+                }
+                for (int g = pd.g0; g < pd.g0 + pd.ng; ++g) {
+                    const GroupDesc& G = plan.groups[g];
+                    for (int tid = 0; tid < nt; ++tid) {
+                        uint32_t base = 0;
+                        for (int m = 0; m < tb; ++m)
+                            if ((tid >> m) & 1) base ^= G.tcol[m];
+                        cd a[16];
+                        for (int j = 0; j < 16; ++j) a[j] = tile[base ^ G.combo[j]];
+                        for (int r = 0; r < kRegBits; ++r) {
+                            if (G.mat[r] < 0) continue;
+                            const double* M = mats.data() + (size_t)(pd.m0 + G.mat[r]) * 8;
+                            const cd m00(M[0], M[1]), m01(M[2], M[3]), m10(M[4], M[5]), m11(M[6], M[7]);
+                            for (int j = 0; j < 16; ++j) {
+                                if ((j >> r) & 1) continue;
+                                const cd u = a[j], v = a[j | (1 << r)];
+                                a[j] = m00 * u + m01 * v;
+                                a[j | (1 << r)] = m10 * u + m11 * v;
+                            }
+                        }
+                        for (int j = 0; j < 16; ++j) tile[base ^ G.combo[j]] = a[j];
+                    }
+                }
+                for (int tid = 0; tid < nt; ++tid) {
+                    uint32_t fs = 0;
+                    uint64_t tg = 0;
+                    for (int j = 0; j < tb; ++j)
+                        if ((tid >> j) & 1) { fs ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
+                    for (int it = 0; it < 16; ++it) st[outer | tg | pd.g_hi[it]] = tile[fs ^ pd.fin_hi[it]];
+                }
+            }
+        }
+        for (size_t i = 0; i < ((size_t)1 << n); ++i) { out[2 * i] = st[i].real(); out[2 * i + 1] = st[i].imag(); }
+        return (int)plan.pdesc.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// Plan shape: stats[0] passes, [1] groups, [2] matrix slots, [3] fused ops,
+// [4] tile bits, [5] single tile; per-pass matrices in pass_mats (if non-null, <= cap).
+int qvp_plan_stats(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1, int precision,
+                   int max_tile_bits, int64_t* stats, int32_t* pass_mats, int32_t cap) {
+    try {
+        const Topology topo = make_topo(n, n_gates, kinds, q0, q1);
+        const Plan plan = build_plan(topo, precision, max_tile_bits);
+        stats[0] = (int64_t)plan.pdesc.size();
+        stats[1] = (int64_t)plan.groups.size();
+        stats[2] = plan.n_slots();
+        stats[3] = (int64_t)plan.ops.size();
+        stats[4] = plan.k;
+        stats[5] = plan.single_tile ? 1 : 0;
+        if (pass_mats)
+            for (size_t p = 0; p < plan.pdesc.size() && (int32_t)p < cap; ++p) pass_mats[p] = plan.pdesc[p].nm;
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,792 @@
+// qvb200.cu — executor runtime and the C ABI declared in include/qvb200.h.
+//
+// One `Engine` per qv_handle: a CUDA device, a stream, a plan cache keyed by
+// circuit topology, grow-only device buffers and the prefix-sharing scheduler.
+//
+// Scheduler (large registers, state in HBM).  A parameter-shift batch
+// (reference gradients.py:33-46) is 2*N_theta copies of one circuit that each
+// differ in one angle.  Every circuit is a fixed sequence of plan passes whose
+// inputs are the previous pass's output and this circuit's fused matrices, so
+// two circuits whose matrices agree on passes [0, p) have bit-identical states
+// after pass p-1.  The scheduler keeps one "trunk" state (the prefix shared by
+// the most circuits), branches every circuit off the trunk at the first pass
+// where it differs, and runs the branches in batches on work buffers.  The
+// arithmetic each circuit sees is exactly what it would see alone, so results
+// stay bitwise independent of batch composition and device (pool.py:10-14),
+// while the number of HBM sweeps drops to sum_c (P - branch_pass_c).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+#include "qvb200.h"
+
+namespace qvb {
+
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ArgError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CircuitError : std::runtime_error {
+    int64_t index;
+    CircuitError(int64_t i, const std::string& m) : std::runtime_error(m), index(i) {}
+};
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename X>
+struct DevBuf {
+    X* p = nullptr;
+    size_t cap = 0;
+    X* get(size_t n) {
+        if (n == 0) n = 1;
+        if (n > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, n * sizeof(X)));
+            cap = n;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct CachedPlan {
+    Topology topo;
+    Plan plan;
+    DevBuf<GroupDesc> d_groups;
+};
+
+constexpr int kNT128 = 256;   // threads per CTA at k = 12, complex128
+constexpr int kNT64 = 512;    // threads per CTA at k = 13, complex64
+
+uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < bytes; ++i) { h ^= p[i]; h *= 1099511628211ull; }
+    return h;
+}
+
+struct Engine {
+    int device = 0;
+    int precision = 0;
+    uint64_t budget = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    std::string err;
+    int64_t err_circuit = -1;
+    double stats[16] = {0};
+    std::unordered_map<std::string, std::unique_ptr<CachedPlan>> plans;
+
+    DevBuf<unsigned char> d_states;
+    DevBuf<unsigned char> d_mats;
+    DevBuf<LaunchEntry> d_entries;
+    DevBuf<double> d_partial;
+    DevBuf<double2> d_partial2;
+    DevBuf<double> d_sup_out, d_js_out, d_full_out, d_pauli_out, d_target;
+    DevBuf<uint64_t> d_support, d_tflip, d_tphase;
+    DevBuf<int64_t> d_term_off, d_slots;
+    DevBuf<int32_t> d_sup_off, d_sup_local, d_sup_pos;
+    std::vector<cudaEvent_t> events;
+    size_t events_used = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;   // pass-kernel (start, stop) of this call
+
+    size_t amp_bytes() const { return precision == 0 ? 16 : 8; }
+    size_t mat_scalar_bytes() const { return precision == 0 ? 8 : 4; }
+
+    cudaEvent_t next_event() {
+        if (events_used == events.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            events.push_back(e);
+        }
+        return events[events_used++];
+    }
+};
+
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Request {   // one qv_execute call, validated
+    const qv_circuits* c;
+    const qv_results* r;
+    int n;
+    int64_t C;
+};
+
+void validate(const Request& q) {
+    const qv_circuits* c = q.c;
+    if (c->n_qubits < 1 || c->n_qubits > kMaxQubits) throw ArgError("n_qubits must be in 1.." + std::to_string(kMaxQubits));
+    if (c->n_circuits < 1) throw ArgError("empty batch");
+    if (!c->kinds || !c->q0 || !c->q1 || !c->angles) throw ArgError("null gate arrays");
+    if (!c->uniform && !c->gate_offsets) throw ArgError("gate_offsets required when uniform = 0");
+    const int n = c->n_qubits;
+    auto check_gate = [&](int64_t ci, uint8_t k, int32_t a, int32_t b, double ang) {
+        if (k > QV_GATE_CZ) throw CircuitError(ci, "unsupported gate kind " + std::to_string(k));
+        if (k == QV_GATE_MEASURE_ALL) return;
+        if (a < 0 || a >= n) throw CircuitError(ci, "gate targets qubit " + std::to_string(a) + " on " + std::to_string(n) + " qubits");
+        if (k == QV_GATE_CNOT || k == QV_GATE_CZ) {
+            if (b < 0 || b >= n) throw CircuitError(ci, "gate targets qubit " + std::to_string(b) + " on " + std::to_string(n) + " qubits");
+            if (a == b) throw CircuitError(ci, "repeated qubit index in two-qubit gate");
+        }
+        if ((k == QV_GATE_RY || k == QV_GATE_RZ || k == QV_GATE_RX) && !std::isfinite(ang))
+            throw CircuitError(ci, "non-finite angle");
+    };
+    if (c->uniform) {
+        if (c->n_gates < 0) throw ArgError("n_gates < 0");
+        for (int64_t g = 0; g < c->n_gates; ++g) {
+            const uint8_t k = c->kinds[g];
+            if (k > QV_GATE_CZ || k == QV_GATE_MEASURE_ALL) { check_gate(0, k, c->q0[g], c->q1[g], 0.0); continue; }
+            check_gate(0, k, c->q0[g], c->q1[g], 0.0);
+            if (k == QV_GATE_RY || k == QV_GATE_RZ || k == QV_GATE_RX)
+                for (int64_t ci = 0; ci < q.C; ++ci)
+                    if (!std::isfinite(c->angles[ci * c->n_gates + g])) throw CircuitError(ci, "non-finite angle");
+        }
+    } else {
+        for (int64_t ci = 0; ci < q.C; ++ci) {
+            const int64_t g0 = c->gate_offsets[ci], g1 = c->gate_offsets[ci + 1];
+            if (g1 < g0) throw ArgError("gate_offsets must be non-decreasing");
+            for (int64_t g = g0; g < g1; ++g) check_gate(ci, c->kinds[g], c->q0[g], c->q1[g], c->angles[g]);
+        }
+    }
+    const qv_results* r = q.r;
+    if (r->kind < QV_OUT_PAULI || r->kind > QV_OUT_JS) throw ArgError("unknown result kind");
+    const uint64_t full = n >= 64 ? ~0ull : ((1ull << n) - 1);
+    if (r->kind == QV_OUT_PAULI) {
+        if (!r->term_offsets || !r->xmask || !r->ymask || !r->zmask) throw ArgError("null Pauli arrays");
+        for (int64_t ci = 0; ci < q.C; ++ci) {
+            const int64_t t0 = r->term_offsets[ci], t1 = r->term_offsets[ci + 1];
+            if (t1 < t0) throw ArgError("term_offsets must be non-decreasing");
+            for (int64_t t = t0; t < t1; ++t) {
+                const uint64_t x = r->xmask[t], y = r->ymask[t], z = r->zmask[t];
+                if ((x | y | z) & ~full) throw CircuitError(ci, "term acts on a qubit beyond the register");
+                if ((x & y) | (x & z) | (y & z)) throw ArgError("overlapping Pauli masks");
+            }
+        }
+    } else if (r->kind == QV_OUT_SUPPORT || r->kind == QV_OUT_JS) {
+        if (r->support_count < 0 || (r->support_count > 0 && !r->support)) throw ArgError("bad support");
+        if (r->kind == QV_OUT_JS && r->support_count > 0 && !r->target) throw ArgError("JS needs target probabilities");
+        for (int64_t s = 0; s < r->support_count; ++s) {
+            if (r->support[s] & ~full) throw ArgError("support index beyond the register");
+            if (s && r->support[s] <= r->support[s - 1]) throw ArgError("support must be sorted and unique");
+        }
+    } else if (r->kind == QV_OUT_FULL) {
+        if (n > 24) throw ArgError("full distributions are limited to 24 qubits");
+    }
+}
+
+int64_t output_size(const qv_circuits* c, const qv_results* r) {
+    switch (r->kind) {
+        case QV_OUT_PAULI: return r->term_offsets ? r->term_offsets[c->n_circuits] : -1;
+        case QV_OUT_SUPPORT: return (int64_t)c->n_circuits * (r->support_count + 1);
+        case QV_OUT_FULL: return (int64_t)c->n_circuits << c->n_qubits;
+        case QV_OUT_JS: return c->n_circuits;
+        default: return -1;
+    }
+}
+
+template <typename F>
+void parallel_for(int64_t count, F fn) {
+    const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t nthr = std::min<int64_t>(std::min<int64_t>(hw, 16), std::max<int64_t>(1, count / 16));
+    if (nthr <= 1) { for (int64_t i = 0; i < count; ++i) fn(i); return; }
+    std::vector<std::thread> th;
+    std::atomic<int64_t> next(0);
+    for (int64_t t = 0; t < nthr; ++t)
+        th.emplace_back([&]() {
+            for (;;) {
+                const int64_t i0 = next.fetch_add(8);
+                if (i0 >= count) break;
+                for (int64_t i = i0; i < std::min(count, i0 + 8); ++i) fn(i);
+            }
+        });
+    for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct GroupRun {
+    Engine& E;
+    const Request& q;
+    CachedPlan& cp;
+    std::vector<int64_t> circuits;          // batch indices in this topology group
+    std::vector<const double*> angle_rows;  // per circuit, indexed by topology gate
+    double* out;                            // caller output
+
+    // unique states
+    std::vector<int64_t> uniq_of;            // per circuit -> unique id
+    std::vector<int64_t> uniq_rep;           // unique -> representative circuit (local index)
+    std::vector<double> hmats;               // [C][slots*8] double
+    size_t slots8 = 0;
+
+    template <typename T>
+    void run();
+};
+
+template <typename T>
+void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const LaunchEntry* d_ent, int nstates,
+                 int64_t ntiles, const EpiArgs& ep, bool timed) {
+    typedef typename Cx<T>::V V;
+    constexpr int NT = sizeof(T) == 8 ? kNT128 : kNT64;
+    const size_t smem = (sizeof(V) << pd.k) + (size_t)pd.ng * sizeof(GroupDesc) + (size_t)pd.nm * 8 * sizeof(T) + 32 * sizeof(double);
+    const int threads = std::max(32, 1 << (pd.k - kRegBits));
+    const int64_t blocks = ntiles * nstates;
+    if (blocks > 0x7fffffffll) throw ArgError("launch too large");
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) { e0 = E.next_event(); e1 = E.next_event(); CK(cudaEventRecord(e0, E.stream)); }
+    pass_kernel<T, NT><<<(unsigned)blocks, threads, smem, E.stream>>>(pd, d_groups, d_ent, nstates, ep);
+    CK(cudaGetLastError());
+    if (timed) { CK(cudaEventRecord(e1, E.stream)); E.timed.push_back({e0, e1}); }
+    E.stats[0] += 1;
+}
+
+template <typename T>
+void GroupRun::run() {
+    typedef typename Cx<T>::V V;
+    const Plan& plan = cp.plan;
+    const Topology& topo = cp.topo;
+    const int n = q.n;
+    const int64_t C = (int64_t)circuits.size();
+    const int slots = plan.n_slots();
+    slots8 = (size_t)slots * 8;
+    const qv_results* R = q.r;
+    const int P = (int)plan.pdesc.size();
+
+    // 1. fused matrices per circuit (host, FP64)
+    hmats.assign((size_t)C * slots8, 0.0);
+    parallel_for(C, [&](int64_t i) { circuit_matrices(plan, topo, angle_rows[i], hmats.data() + (size_t)i * slots8); });
+
+    // 2. deduplicate identical circuits (same topology + same matrices)
+    uniq_of.assign(C, -1);
+    uniq_rep.clear();
+    {
+        std::unordered_map<uint64_t, std::vector<int64_t>> seen;
+        for (int64_t i = 0; i < C; ++i) {
+            const double* row = hmats.data() + (size_t)i * slots8;
+            const uint64_t h = fnv1a(row, slots8 * sizeof(double));
+            auto& cand = seen[h];
+            int64_t u = -1;
+            for (int64_t j : cand) {
+                if (!std::memcmp(row, hmats.data() + (size_t)uniq_rep[j] * slots8, slots8 * sizeof(double))) { u = j; break; }
+            }
+            if (u < 0) { u = (int64_t)uniq_rep.size(); uniq_rep.push_back(i); cand.push_back(u); }
+            uniq_of[i] = u;
+        }
+    }
+    const int64_t U = (int64_t)uniq_rep.size();
+    E.stats[3] += (double)U;
+
+    // 3. matrices of unique states on the device (precision of the state)
+    std::vector<T> umats((size_t)U * slots8);
+    for (int64_t u = 0; u < U; ++u) {
+        const double* src = hmats.data() + (size_t)uniq_rep[u] * slots8;
+        for (size_t j = 0; j < slots8; ++j) umats[(size_t)u * slots8 + j] = (T)src[j];
+    }
+    T* d_mats = reinterpret_cast<T*>(E.d_mats.get(std::max<size_t>(1, umats.size()) * sizeof(T)));
+    if (!umats.empty()) CK(cudaMemcpyAsync(d_mats, umats.data(), umats.size() * sizeof(T), cudaMemcpyHostToDevice, E.stream));
+
+    // 4. result plumbing per unique state
+    EpiArgs ep;
+    std::memset(&ep, 0, sizeof(ep));
+    ep.n = n;
+    ep.S = (R->kind == QV_OUT_SUPPORT || R->kind == QV_OUT_JS) ? R->support_count : 0;
+    std::vector<int64_t> term_off_u;     // per unique: offsets into unique-term arrays
+    std::vector<int64_t> uterm_src;      // unique term -> caller term index
+    if (R->kind == QV_OUT_PAULI) {
+        std::vector<std::vector<int64_t>> per_u(U);
+        for (int64_t i = 0; i < C; ++i) {
+            const int64_t ci = circuits[i];
+            for (int64_t t = R->term_offsets[ci]; t < R->term_offsets[ci + 1]; ++t) per_u[uniq_of[i]].push_back(t);
+        }
+        term_off_u.push_back(0);
+        for (int64_t u = 0; u < U; ++u) {
+            for (int64_t t : per_u[u]) uterm_src.push_back(t);
+            term_off_u.push_back((int64_t)uterm_src.size());
+        }
+        const int64_t NTm = (int64_t)uterm_src.size();
+        std::vector<uint64_t> fl(NTm), ph(NTm);
+        for (int64_t j = 0; j < NTm; ++j) {
+            const int64_t t = uterm_src[j];
+            fl[j] = R->xmask[t] | R->ymask[t];
+            ph[j] = R->ymask[t] | R->zmask[t];
+        }
+        uint64_t* dfl = E.d_tflip.get(NTm);
+        uint64_t* dph = E.d_tphase.get(NTm);
+        int64_t* dto = E.d_term_off.get(U + 1);
+        if (NTm) {
+            CK(cudaMemcpyAsync(dfl, fl.data(), NTm * 8, cudaMemcpyHostToDevice, E.stream));
+            CK(cudaMemcpyAsync(dph, ph.data(), NTm * 8, cudaMemcpyHostToDevice, E.stream));
+        }
+        CK(cudaMemcpyAsync(dto, term_off_u.data(), (U + 1) * 8, cudaMemcpyHostToDevice, E.stream));
+        ep.term_off = dto;
+        ep.t_flip = dfl;
+        ep.t_phase = dph;
+        ep.pauli_out = E.d_pauli_out.get(NTm);
+    }
+    if (ep.S > 0) {
+        uint64_t* dsu = E.d_support.get(ep.S);
+        CK(cudaMemcpyAsync(dsu, R->support, ep.S * 8, cudaMemcpyHostToDevice, E.stream));
+        ep.support = dsu;
+        if (R->kind == QV_OUT_JS) {
+            double* dta = E.d_target.get(ep.S);
+            CK(cudaMemcpyAsync(dta, R->target, ep.S * 8, cudaMemcpyHostToDevice, E.stream));
+            ep.target = dta;
+        }
+    }
+    ep.sup_out = E.d_sup_out.get((size_t)U * (ep.S + 1));
+    ep.js_out = E.d_js_out.get(U);
+    if (R->kind == QV_OUT_FULL) ep.full_out = E.d_full_out.get((size_t)U << n);
+
+    const size_t state_bytes = sizeof(V) << n;
+    cudaEvent_t call0 = E.next_event();
+    CK(cudaEventRecord(call0, E.stream));
+
+    if (plan.single_tile) {
+        // whole register in one CTA's shared memory: one launch for the batch
+        std::vector<LaunchEntry> ents(U);
+        for (int64_t u = 0; u < U; ++u) ents[u] = {nullptr, nullptr, d_mats + (size_t)u * slots8, u, 0, 0};
+        LaunchEntry* dent = E.d_entries.get(U);
+        CK(cudaMemcpyAsync(dent, ents.data(), U * sizeof(LaunchEntry), cudaMemcpyHostToDevice, E.stream));
+        ep.flags = F_SINGLE;
+        if (R->kind == QV_OUT_PAULI) ep.flags |= F_S_PAULI;
+        if (R->kind == QV_OUT_SUPPORT) ep.flags |= F_S_SUPPORT;
+        if (R->kind == QV_OUT_JS) ep.flags |= F_S_JS;
+        if (R->kind == QV_OUT_FULL) ep.flags |= F_S_FULL;
+        ep.ntiles = 1;
+        if (U > 0x7fffffffll) throw ArgError("batch too large");
+        launch_pass<T>(E, plan.pdesc[0], cp.d_groups.p, dent, (int)U, 1, ep, true);
+        E.stats[1] += (double)U;
+        E.stats[2] += (double)C;
+    } else {
+        const int k = plan.k;
+        const int64_t ntiles = 1ll << (n - k);
+        ep.ntiles = ntiles;
+        // support CSR over the last pass's tiles
+        const PassDesc& last = plan.pdesc[P - 1];
+        if (ep.S > 0) {
+            int pos_of_bit[64];
+            for (int b = 0; b < 64; ++b) pos_of_bit[b] = -1;
+            std::vector<int32_t> cnt(ntiles + 1, 0), local(ep.S), tile_of(ep.S);
+            for (int64_t s = 0; s < ep.S; ++s) {
+                const uint64_t g = R->support[s];
+                uint32_t loc = 0;
+                uint64_t tl = 0;
+                for (int j = 0; j < k; ++j)
+                    if ((g >> last.sbits[j]) & 1) loc |= 1u << j;
+                for (int j = 0; j < last.n_outer; ++j)
+                    if ((g >> last.obits[j]) & 1) tl |= 1ull << j;
+                local[s] = (int32_t)loc;
+                tile_of[s] = (int32_t)tl;
+                cnt[tl + 1]++;
+            }
+            (void)pos_of_bit;
+            for (int64_t t = 0; t < ntiles; ++t) cnt[t + 1] += cnt[t];
+            std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1), sl(ep.S), sp(ep.S);
+            for (int64_t s = 0; s < ep.S; ++s) {
+                const int32_t at = fill[tile_of[s]]++;
+                sl[at] = local[s];
+                sp[at] = (int32_t)s;
+            }
+            int32_t* doff = E.d_sup_off.get(ntiles + 1);
+            int32_t* dloc = E.d_sup_local.get(ep.S);
+            int32_t* dpos = E.d_sup_pos.get(ep.S);
+            CK(cudaMemcpyAsync(doff, cnt.data(), (ntiles + 1) * 4, cudaMemcpyHostToDevice, E.stream));
+            CK(cudaMemcpyAsync(dloc, sl.data(), ep.S * 4, cudaMemcpyHostToDevice, E.stream));
+            CK(cudaMemcpyAsync(dpos, sp.data(), ep.S * 4, cudaMemcpyHostToDevice, E.stream));
+            ep.sup_off = doff;
+            ep.sup_local = dloc;
+            ep.sup_pos = dpos;
+        }
+        const bool dist = R->kind == QV_OUT_SUPPORT || R->kind == QV_OUT_JS;
+        const bool need_state_out = !dist;   // Pauli / full read the stored state
+
+        // pass signatures per unique state
+        std::vector<std::vector<uint64_t>> sig(U, std::vector<uint64_t>(P));
+        for (int64_t u = 0; u < U; ++u)
+            for (int p = 0; p < P; ++p)
+                sig[u][p] = fnv1a(umats.data() + (size_t)u * slots8 + (size_t)plan.pdesc[p].m0 * 8,
+                                  (size_t)plan.pdesc[p].nm * 8 * sizeof(T), 0x9e3779b97f4a7c15ull + p);
+        auto same_pass = [&](int64_t a, int64_t b, int p) {
+            if (sig[a][p] != sig[b][p]) return false;
+            const size_t off = (size_t)plan.pdesc[p].m0 * 8, len = (size_t)plan.pdesc[p].nm * 8 * sizeof(T);
+            return !std::memcmp(umats.data() + (size_t)a * slots8 + off, umats.data() + (size_t)b * slots8 + off, len);
+        };
+
+        // memory: trunk + W work states
+        const bool need_trunk = P > 1 && U > 1;
+        const uint64_t avail_states = E.budget / state_bytes;
+        if (avail_states < (need_trunk ? 2u : 1u))
+            throw ArgError("a " + std::to_string(n) + "-qubit state (" + std::to_string(state_bytes >> 20) +
+                           " MiB) does not fit the memory budget");
+        int64_t W = (int64_t)avail_states - (need_trunk ? 1 : 0);
+        W = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(W, 64), U));
+        unsigned char* base = E.d_states.get((size_t)(W + (need_trunk ? 1 : 0)) * state_bytes);
+        V* trunk = need_trunk ? reinterpret_cast<V*>(base) : nullptr;
+        auto work = [&](int64_t b) { return reinterpret_cast<V*>(base + (size_t)((need_trunk ? 1 : 0) + b) * state_bytes); };
+        double* partial = E.d_partial.get((size_t)W * ntiles);
+
+        // ---- build the whole launch schedule on the host -----------------
+        enum LKind { L_PASS, L_FINAL_DIST, L_FULL, L_PAULI };
+        struct L {
+            LKind kind;
+            int pass;
+            size_t off;     // entries (L_PASS) / slot pairs (L_FINAL_DIST)
+            int count;      // states
+            int flags;
+            V* state;       // L_FULL / L_PAULI
+            int64_t u, j;   // unique id / unique term
+            double bytes;
+        };
+        std::vector<L> sched;
+        std::vector<LaunchEntry> ents;
+        std::vector<int64_t> slots_tab;
+
+        auto run_chains = [&](const std::vector<int64_t>& D, int p) {
+            for (size_t b0 = 0; b0 < D.size(); b0 += (size_t)W) {
+                const int nb = (int)std::min<size_t>((size_t)W, D.size() - b0);
+                for (int pp = p; pp < P; ++pp) {
+                    const bool lastp = pp == P - 1;
+                    const size_t off = ents.size();
+                    for (int b = 0; b < nb; ++b) {
+                        const int64_t u = D[b0 + b];
+                        const void* in = pp == p ? (p == 0 ? nullptr : (const void*)trunk) : (const void*)work(b);
+                        void* o = (lastp && !need_state_out) ? nullptr : (void*)work(b);
+                        ents.push_back({in, o, d_mats + (size_t)u * slots8, u, b, 0});
+                    }
+                    int flags = F_STORE;
+                    if (lastp && dist) flags = F_NORM | F_SUPPORT;
+                    if (lastp && R->kind == QV_OUT_FULL) flags = F_STORE | F_NORM;
+                    const double rd = (pp == p && p == 0) ? 0.0 : 1.0, wr = (flags & F_STORE) ? 1.0 : 0.0;
+                    sched.push_back({L_PASS, pp, off, nb, flags, nullptr, 0, 0, nb * (double)state_bytes * (rd + wr)});
+                }
+                if (dist || R->kind == QV_OUT_FULL) {
+                    const size_t off = slots_tab.size();
+                    for (int b = 0; b < nb; ++b) { slots_tab.push_back(D[b0 + b]); slots_tab.push_back(b); }
+                    sched.push_back({L_FINAL_DIST, 0, off, nb, 0, nullptr, 0, 0, 0});
+                    if (R->kind == QV_OUT_FULL)
+                        for (int b = 0; b < nb; ++b) sched.push_back({L_FULL, 0, 0, 1, 0, work(b), D[b0 + b], 0, 0});
+                } else {
+                    for (int b = 0; b < nb; ++b) {
+                        const int64_t u = D[b0 + b];
+                        for (int64_t j = term_off_u[u]; j < term_off_u[u + 1]; ++j)
+                            sched.push_back({L_PAULI, 0, 0, 1, 0, work(b), u, j, 0});
+                    }
+                }
+            }
+        };
+
+        std::vector<int64_t> alive(U);
+        for (int64_t u = 0; u < U; ++u) alive[u] = u;
+        for (int p = 0; p < P && !alive.empty(); ++p) {
+            // the largest class of alive states sharing pass p stays on the trunk
+            std::vector<std::vector<int64_t>> classes;
+            std::unordered_map<uint64_t, std::vector<size_t>> by_sig;
+            for (int64_t u : alive) {
+                auto& cand = by_sig[sig[u][p]];
+                bool placed = false;
+                for (size_t ci : cand)
+                    if (same_pass(classes[ci][0], u, p)) { classes[ci].push_back(u); placed = true; break; }
+                if (!placed) { cand.push_back(classes.size()); classes.push_back({u}); }
+            }
+            size_t best = 0;
+            for (size_t i = 1; i < classes.size(); ++i)
+                if (classes[i].size() > classes[best].size()) best = i;
+            if (classes[best].size() <= 1 || !need_trunk) {
+                run_chains(alive, p);
+                alive.clear();
+                break;
+            }
+            std::vector<int64_t> stay = classes[best], D;
+            std::vector<char> in_stay(U, 0);
+            for (int64_t u : stay) in_stay[u] = 1;
+            for (int64_t u : alive)
+                if (!in_stay[u]) D.push_back(u);
+            if (!D.empty()) run_chains(D, p);
+            alive.swap(stay);
+            const size_t off = ents.size();
+            ents.push_back({p == 0 ? nullptr : (const void*)trunk, (void*)trunk, d_mats + (size_t)alive[0] * slots8, alive[0], 0, 0});
+            sched.push_back({L_PASS, p, off, 1, F_STORE, nullptr, 0, 0, (double)state_bytes * ((p == 0 ? 0 : 1) + 1)});
+        }
+        if (!alive.empty()) throw std::runtime_error("scheduler left states unfinished");
+
+        // ---- upload tables once, then issue every launch -----------------
+        LaunchEntry* dent = E.d_entries.get(ents.size());
+        CK(cudaMemcpyAsync(dent, ents.data(), ents.size() * sizeof(LaunchEntry), cudaMemcpyHostToDevice, E.stream));
+        int64_t* dslots = E.d_slots.get(std::max<size_t>(2, slots_tab.size()));
+        if (!slots_tab.empty())
+            CK(cudaMemcpyAsync(dslots, slots_tab.data(), slots_tab.size() * 8, cudaMemcpyHostToDevice, E.stream));
+        for (const L& l : sched) {
+            if (l.kind == L_PASS) {
+                EpiArgs e2 = ep;
+                e2.flags = l.flags;
+                e2.partial = partial;
+                if (!(l.flags & F_SUPPORT)) e2.sup_off = nullptr;
+                launch_pass<T>(E, plan.pdesc[l.pass], cp.d_groups.p, dent + l.off, l.count, ntiles, e2, true);
+                E.stats[1] += l.count;
+                E.stats[4] += l.bytes;
+            } else if (l.kind == L_FINAL_DIST) {
+                finalize_dist_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, ntiles, partial, ep.sup_out, ep.S,
+                                                                     ep.target, ep.js_out, R->kind == QV_OUT_JS);
+                CK(cudaGetLastError());
+                E.stats[0] += 1;
+            } else if (l.kind == L_FULL) {
+                full_probs_kernel<T><<<1184, 256, 0, E.stream>>>(l.state, 1ll << n, ep.sup_out + l.u * (ep.S + 1) + ep.S,
+                                                                 ep.full_out + ((size_t)l.u << n));
+                CK(cudaGetLastError());
+                E.stats[0] += 1;
+            } else {
+                const int64_t t = uterm_src[l.j];
+                const uint64_t F = R->xmask[t] | R->ymask[t], PH = R->ymask[t] | R->zmask[t];
+                const int64_t count = F ? (1ll << (n - 1)) : (1ll << n);
+                const int64_t per_block = std::min<int64_t>(count, 8192);
+                const int64_t nblk = count / per_block;
+                double2* p2 = E.d_partial2.get(std::max<int64_t>(nblk, 1 << 20));
+                pauli_sweep_kernel<T><<<(unsigned)nblk, 256, 0, E.stream>>>(l.state, n, F, PH, per_block, p2);
+                CK(cudaGetLastError());
+                finalize_pauli_kernel<<<1, 1024, 0, E.stream>>>(p2, nblk, __builtin_popcountll(R->ymask[t]), ep.pauli_out + l.j);
+                CK(cudaGetLastError());
+                E.stats[0] += 2;
+            }
+        }
+        if (!alive.empty()) throw std::runtime_error("scheduler left states unfinished");
+        E.stats[2] += (double)C * P;
+    }
+    cudaEvent_t call1 = E.next_event();
+    CK(cudaEventRecord(call1, E.stream));
+
+    // 5. results back to the caller, circuit by circuit
+    CK(cudaStreamSynchronize(E.stream));
+    float call_ms = 0.f;
+    CK(cudaEventElapsedTime(&call_ms, call0, call1));
+    E.stats[8] += call_ms;
+    if (R->kind == QV_OUT_PAULI) {
+        std::vector<double> vals(uterm_src.size());
+        if (!vals.empty()) CK(cudaMemcpy(vals.data(), ep.pauli_out, vals.size() * 8, cudaMemcpyDeviceToHost));
+        for (size_t j = 0; j < uterm_src.size(); ++j) out[uterm_src[j]] = vals[j];
+    } else if (R->kind == QV_OUT_SUPPORT) {
+        const size_t row = (size_t)ep.S + 1;
+        std::vector<double> vals((size_t)U * row);
+        CK(cudaMemcpy(vals.data(), ep.sup_out, vals.size() * 8, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < C; ++i)
+            std::memcpy(out + (size_t)circuits[i] * row, vals.data() + (size_t)uniq_of[i] * row, row * 8);
+    } else if (R->kind == QV_OUT_JS) {
+        std::vector<double> vals(U);
+        CK(cudaMemcpy(vals.data(), ep.js_out, U * 8, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < C; ++i) out[circuits[i]] = vals[uniq_of[i]];
+    } else {
+        const size_t row = (size_t)1 << n;
+        std::vector<double> vals((size_t)U * row);
+        CK(cudaMemcpy(vals.data(), ep.full_out, vals.size() * 8, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < C; ++i)
+            std::memcpy(out + (size_t)circuits[i] * row, vals.data() + (size_t)uniq_of[i] * row, row * 8);
+    }
+    E.stats[6] = P;
+    E.stats[7] = plan.k;
+}
+
+CachedPlan& get_plan(Engine& E, Topology&& topo) {
+    const std::string key = topo.key();
+    auto it = E.plans.find(key);
+    if (it != E.plans.end()) return *it->second;
+    auto cp = std::make_unique<CachedPlan>();
+    cp->plan = build_plan(topo, E.precision);
+    cp->topo = std::move(topo);
+    GroupDesc* d = cp->d_groups.get(std::max<size_t>(1, cp->plan.groups.size()));
+    if (!cp->plan.groups.empty())
+        CK(cudaMemcpy(d, cp->plan.groups.data(), cp->plan.groups.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice));
+    CachedPlan& ref = *cp;
+    E.plans.emplace(key, std::move(cp));
+    return ref;
+}
+
+void execute(Engine& E, const qv_circuits* c, const qv_results* r, double* out, int64_t out_len) {
+    Request q{c, r, c ? c->n_qubits : 0, c ? c->n_circuits : 0};
+    if (!c || !r || !out) throw ArgError("null argument");
+    validate(q);
+    const int64_t need = output_size(c, r);
+    if (need < 0 || out_len < need) throw ArgError("output buffer too small: need " + std::to_string(need));
+    CK(cudaSetDevice(E.device));
+    std::memset(E.stats, 0, sizeof(E.stats));
+    E.events_used = 0;
+    E.timed.clear();
+    const int n = c->n_qubits;
+
+    auto topo_of = [&](int64_t ci) {
+        Topology t;
+        t.n = n;
+        const int64_t g0 = c->uniform ? 0 : c->gate_offsets[ci];
+        const int64_t g1 = c->uniform ? c->n_gates : c->gate_offsets[ci + 1];
+        t.kind.assign(c->kinds + g0, c->kinds + g1);
+        t.q0.assign(c->q0 + g0, c->q0 + g1);
+        t.q1.assign(c->q1 + g0, c->q1 + g1);
+        for (size_t g = 0; g < t.kind.size(); ++g)
+            if (!is_two_qubit(t.kind[g])) t.q1[g] = -1;
+        return t;
+    };
+    // group circuits by topology (a uniform batch is one group)
+    std::vector<std::pair<CachedPlan*, std::vector<int64_t>>> groups;
+    if (c->uniform) {
+        std::vector<int64_t> all(c->n_circuits);
+        for (int64_t i = 0; i < c->n_circuits; ++i) all[i] = i;
+        groups.push_back({&get_plan(E, topo_of(0)), std::move(all)});
+    } else {
+        std::unordered_map<std::string, size_t> index;
+        for (int64_t ci = 0; ci < c->n_circuits; ++ci) {
+            Topology t = topo_of(ci);
+            const std::string key = t.key();
+            auto it = index.find(key);
+            if (it == index.end()) {
+                index.emplace(key, groups.size());
+                groups.push_back({&get_plan(E, std::move(t)), {ci}});
+            } else {
+                groups[it->second].second.push_back(ci);
+            }
+        }
+    }
+    for (auto& g : groups) {
+        GroupRun run{E, q, *g.first, g.second, {}, out};
+        run.angle_rows.resize(g.second.size());
+        for (size_t i = 0; i < g.second.size(); ++i) {
+            const int64_t ci = g.second[i];
+            run.angle_rows[i] = c->uniform ? c->angles + ci * c->n_gates : c->angles + c->gate_offsets[ci];
+        }
+        if (E.precision == 0) run.run<double>();
+        else run.run<float>();
+    }
+    // device time of pass kernels (event pairs recorded by launch_pass; the
+    // stream was synchronised when the results were copied back)
+    double ms = 0;
+    for (auto& pr : E.timed) {
+        float x = 0.f;
+        CK(cudaEventElapsedTime(&x, pr.first, pr.second));
+        ms += x;
+    }
+    E.stats[5] = ms;
+}
+
+}  // namespace qvb
+
+// ---------------------------------------------------------------------------
+using namespace qvb;
+
+extern "C" {
+
+const char* qv_version(void) { return "qvb200 0.1 sm_100a"; }
+
+int qv_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) return 0;
+    return count;
+}
+
+int64_t qv_output_size(const qv_circuits* circuits, const qv_results* results) {
+    if (!circuits || !results) return -1;
+    return output_size(circuits, results);
+}
+
+int qv_create(int device, int precision, uint64_t memory_budget_bytes, qv_handle* out) {
+    if (!out) return QV_ERR_ARGUMENT;
+    *out = nullptr;
+    if (precision != QV_COMPLEX128 && precision != QV_COMPLEX64) return QV_ERR_ARGUMENT;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return QV_ERR_CUDA;
+    if (device < 0 || device >= count) return QV_ERR_ARGUMENT;
+    try {
+        auto E = new Engine();
+        E->device = device;
+        E->precision = precision;
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        E->budget = memory_budget_bytes ? memory_budget_bytes : (uint64_t)(0.85 * (double)free_b);
+        CK(cudaFuncSetAttribute(pass_kernel<double, kNT128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(pass_kernel<float, kNT64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        *out = reinterpret_cast<qv_handle>(E);
+        return QV_OK;
+    } catch (const std::exception&) {
+        return QV_ERR_CUDA;
+    }
+}
+
+int qv_destroy(qv_handle h) {
+    if (!h) return QV_ERR_ARGUMENT;
+    Engine* E = reinterpret_cast<Engine*>(h);
+    {
+        std::lock_guard<std::mutex> lk(E->mu);
+        cudaSetDevice(E->device);
+        if (E->stream) cudaStreamSynchronize(E->stream);
+        E->d_states.release(); E->d_mats.release(); E->d_entries.release(); E->d_partial.release();
+        E->d_partial2.release(); E->d_sup_out.release(); E->d_js_out.release(); E->d_full_out.release();
+        E->d_pauli_out.release(); E->d_target.release(); E->d_support.release(); E->d_tflip.release();
+        E->d_tphase.release(); E->d_term_off.release(); E->d_slots.release(); E->d_sup_off.release();
+        E->d_sup_local.release(); E->d_sup_pos.release();
+        for (auto& kv : E->plans) kv.second->d_groups.release();
+        for (auto e : E->events) cudaEventDestroy(e);
+        if (E->stream) cudaStreamDestroy(E->stream);
+    }
+    delete E;
+    return QV_OK;
+}
+
+int qv_execute(qv_handle h, const qv_circuits* circuits, const qv_results* results, double* out, int64_t out_len) {
+    if (!h) return QV_ERR_ARGUMENT;
+    Engine* E = reinterpret_cast<Engine*>(h);
+    std::lock_guard<std::mutex> lk(E->mu);
+    E->err.clear();
+    E->err_circuit = -1;
+    try {
+        execute(*E, circuits, results, out, out_len);
+        return QV_OK;
+    } catch (const CircuitError& e) {
+        E->err = e.what();
+        E->err_circuit = e.index;
+        return QV_ERR_CIRCUIT;
+    } catch (const ArgError& e) {
+        E->err = e.what();
+        return QV_ERR_ARGUMENT;
+    } catch (const CudaError& e) {
+        E->err = e.what();
+        return QV_ERR_CUDA;
+    } catch (const std::exception& e) {
+        E->err = e.what();
+        return QV_ERR_INTERNAL;
+    }
+}
+
+const char* qv_last_error(qv_handle h) {
+    if (!h) return "null handle";
+    return reinterpret_cast<Engine*>(h)->err.c_str();
+}
+
+int64_t qv_last_error_circuit(qv_handle h) {
+    if (!h) return -1;
+    return reinterpret_cast<Engine*>(h)->err_circuit;
+}
+
+int qv_last_stats(qv_handle h, double* stats, int32_t n_stats) {
+    if (!h || !stats) return QV_ERR_ARGUMENT;
+    Engine* E = reinterpret_cast<Engine*>(h);
+    for (int i = 0; i < n_stats && i < 16; ++i) stats[i] = E->stats[i];
+    return QV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+"""ctypes binding of libqvb200.so (include/qvb200.h).
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is visible, `engine()` raises `NativeUnavailable` and the backend
+fails loudly.  ctypes releases the GIL for the duration of every call, so
+per-thread backends (one per virtual QPU) overlap on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libqvb200.so"
+
+QV_OK, QV_ERR_ARGUMENT, QV_ERR_CIRCUIT, QV_ERR_CUDA, QV_ERR_INTERNAL = range(5)
+QV_COMPLEX128, QV_COMPLEX64 = 0, 1
+QV_OUT_PAULI, QV_OUT_SUPPORT, QV_OUT_FULL, QV_OUT_JS = range(4)
+
+PRECISIONS = {"complex128": QV_COMPLEX128, "complex64": QV_COMPLEX64}
+
+# Symbols include/qvb200.h declares (checked by the CPU test suite).
+EXPORTS = ("qv_version", "qv_output_size", "qv_create", "qv_destroy", "qv_execute",
+           "qv_last_error", "qv_last_error_circuit", "qv_last_stats", "qv_device_count")
+
+STAT_NAMES = ("launches", "sweeps", "sweeps_unshared", "unique_states", "pass_bytes",
+              "pass_ms", "passes_per_circuit", "tile_bits", "device_ms")
+
+
+class NativeUnavailable(RuntimeError):
+    """libqvb200.so could not be loaded or no B200 is visible."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, message: str, circuit: int):
+        super().__init__(message)
+        self.code = code
+        self.circuit = circuit
+
+
+class QvCircuits(ctypes.Structure):
+    _fields_ = [("n_qubits", ctypes.c_int32), ("n_circuits", ctypes.c_int32), ("uniform", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("n_gates", ctypes.c_int64),
+                ("gate_offsets", ctypes.c_void_p), ("kinds", ctypes.c_void_p), ("q0", ctypes.c_void_p),
+                ("q1", ctypes.c_void_p), ("angles", ctypes.c_void_p)]
+
+
+class QvResults(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("term_offsets", ctypes.c_void_p),
+                ("xmask", ctypes.c_void_p), ("ymask", ctypes.c_void_p), ("zmask", ctypes.c_void_p),
+                ("support_count", ctypes.c_int64), ("support", ctypes.c_void_p), ("target", ctypes.c_void_p)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library() -> ctypes.CDLL:
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise NativeUnavailable(f"{LIB_PATH} is missing; run __graft_entry__.build()")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            lib.qv_version.restype = ctypes.c_char_p
+            lib.qv_output_size.restype = ctypes.c_int64
+            lib.qv_output_size.argtypes = [ctypes.POINTER(QvCircuits), ctypes.POINTER(QvResults)]
+            lib.qv_create.restype = ctypes.c_int
+            lib.qv_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]
+            lib.qv_destroy.restype = ctypes.c_int
+            lib.qv_destroy.argtypes = [ctypes.c_void_p]
+            lib.qv_execute.restype = ctypes.c_int
+            lib.qv_execute.argtypes = [ctypes.c_void_p, ctypes.POINTER(QvCircuits), ctypes.POINTER(QvResults),
+                                       ctypes.c_void_p, ctypes.c_int64]
+            lib.qv_last_error.restype = ctypes.c_char_p
+            lib.qv_last_error.argtypes = [ctypes.c_void_p]
+            lib.qv_last_error_circuit.restype = ctypes.c_int64
+            lib.qv_last_error_circuit.argtypes = [ctypes.c_void_p]
+            lib.qv_last_stats.restype = ctypes.c_int
+            lib.qv_last_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+            lib.qv_device_count.restype = ctypes.c_int
+            lib.qv_device_count.argtypes = []
+            _lib = lib
+        return _lib
+
+
+def _ptr(a: np.ndarray | None) -> int | None:
+    return None if a is None else a.ctypes.data
+
+
+class Engine:
+    """One native executor (a qv_handle) on one device and precision."""
+
+    def __init__(self, device: int, precision: str = "complex128", memory_budget: int = 0):
+        lib = load_library()
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {tuple(PRECISIONS)}")
+        handle = ctypes.c_void_p()
+        code = lib.qv_create(int(device), PRECISIONS[precision], int(memory_budget), ctypes.byref(handle))
+        if code != QV_OK:
+            raise NativeUnavailable(f"qv_create(device={device}) failed with status {code} (no CUDA device?)")
+        self._lib = lib
+        self._handle = handle
+        self.device = int(device)
+        self.precision = precision
+        self.last_stats: dict[str, float] = {}
+
+    def close(self) -> None:
+        if self._handle:
+            self._lib.qv_destroy(self._handle)
+            self._handle = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order varies
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def execute(self, n_qubits: int, lowered: "LoweredBatch", result_kind: int, *,
+                terms: tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray] | None = None,
+                support: np.ndarray | None = None, target: np.ndarray | None = None) -> np.ndarray:
+        """Run one batch; returns the flat float64 output (layout: qvb200.h)."""
+        c = QvCircuits()
+        c.n_qubits = n_qubits
+        c.n_circuits = lowered.n_circuits
+        c.uniform = 1 if lowered.uniform else 0
+        c.n_gates = lowered.n_gates
+        c.gate_offsets = _ptr(lowered.gate_offsets)
+        c.kinds = _ptr(lowered.kinds)
+        c.q0 = _ptr(lowered.q0)
+        c.q1 = _ptr(lowered.q1)
+        c.angles = _ptr(lowered.angles)
+        r = QvResults()
+        r.kind = result_kind
+        keep = []
+        if terms is not None:
+            off, xm, ym, zm = (np.ascontiguousarray(a) for a in terms)
+            keep += [off, xm, ym, zm]
+            r.term_offsets, r.xmask, r.ymask, r.zmask = _ptr(off), _ptr(xm), _ptr(ym), _ptr(zm)
+        if support is not None:
+            support = np.ascontiguousarray(support, dtype=np.uint64)
+            keep.append(support)
+            r.support_count = support.shape[0]
+            r.support = _ptr(support)
+        if target is not None:
+            target = np.ascontiguousarray(target, dtype=np.float64)
+            keep.append(target)
+            r.target = _ptr(target)
+        size = self._lib.qv_output_size(ctypes.byref(c), ctypes.byref(r))
+        if size < 0:
+            raise ValueError("malformed result request")
+        out = np.empty(max(int(size), 1), dtype=np.float64)
+        code = self._lib.qv_execute(self._handle, ctypes.byref(c), ctypes.byref(r), out.ctypes.data, out.shape[0])
+        stats = np.zeros(len(STAT_NAMES), dtype=np.float64)
+        self._lib.qv_last_stats(self._handle, stats.ctypes.data, stats.shape[0])
+        self.last_stats = dict(zip(STAT_NAMES, stats.tolist()))
+        if code != QV_OK:
+            msg = (self._lib.qv_last_error(self._handle) or b"").decode()
+            raise NativeError(code, msg, int(self._lib.qv_last_error_circuit(self._handle)))
+        return out[:size]
+
+
+class LoweredBatch:
+    """Gate arrays of a batch in the C-ABI layout (qv_circuits)."""
+
+    __slots__ = ("n_circuits", "uniform", "n_gates", "gate_offsets", "kinds", "q0", "q1", "angles")
+
+    def __init__(self, n_circuits, uniform, n_gates, gate_offsets, kinds, q0, q1, angles):
+        self.n_circuits = int(n_circuits)
+        self.uniform = bool(uniform)
+        self.n_gates = int(n_gates)
+        self.gate_offsets = None if gate_offsets is None else np.ascontiguousarray(gate_offsets, dtype=np.int64)
+        self.kinds = np.ascontiguousarray(kinds, dtype=np.uint8)
+        self.q0 = np.ascontiguousarray(q0, dtype=np.int32)
+        self.q1 = np.ascontiguousarray(q1, dtype=np.int32)
+        self.angles = np.ascontiguousarray(angles, dtype=np.float64)
+        if self.kinds.shape[0] == 0:   # keep pointers valid for empty circuits
+            self.kinds = np.zeros(1, np.uint8)
+            self.q0 = np.zeros(1, np.int32)
+            self.q1 = np.zeros(1, np.int32)
+        if self.angles.size == 0:
+            self.angles = np.zeros(1, np.float64)
+
+
+_engines: dict[tuple[int, str], Engine] = {}
+_engines_lock = threading.Lock()
+
+
+def device_count() -> int:
+    return int(load_library().qv_device_count())
+
+
+def engine(device: int, precision: str = "complex128") -> Engine:
+    """Process-wide engine per (device, precision); calls on it serialise."""
+    key = (int(device), precision)
+    with _engines_lock:
+        eng = _engines.get(key)
+        if eng is None:
+            eng = Engine(device, precision)
+            _engines[key] = eng
+        return eng

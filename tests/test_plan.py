@@ -1,0 +1,95 @@
+"""CPU checks of the pass planner (no GPU).
+
+libqvb200_plan.so interprets a plan exactly as the CUDA pass kernel does --
+tile staging through the swizzled slot maps, 16-amplitude register groups,
+CNOTs folded into GF(2) slot maps -- on the host.  Comparing it with the
+oracle on random circuits, with tile sizes small enough to force many
+passes, validates the planner's bookkeeping independently of the GPU.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import statevector as sv
+from paper_2406_03466_b200 import build as qbuild
+from paper_2406_03466_b200.ir import CODE_BY_VALUE
+
+
+@pytest.fixture(scope="module")
+def plan_lib():
+    path = qbuild.build_plancheck()
+    lib = ctypes.CDLL(str(path))
+    lib.qvp_simulate.restype = ctypes.c_int
+    lib.qvp_simulate.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    lib.qvp_plan_stats.restype = ctypes.c_int
+    lib.qvp_plan_stats.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+    return lib
+
+
+def arrays(gates):
+    kinds = np.array([CODE_BY_VALUE[k] for k, _, _ in gates] or [0], np.uint8)
+    q0 = np.array([t[0] if t else 0 for _, t, _ in gates] or [0], np.int32)
+    q1 = np.array([t[1] if len(t) > 1 else -1 for _, t, _ in gates] or [0], np.int32)
+    ang = np.array([a if a is not None else 0.0 for _, _, a in gates] or [0.0], np.float64)
+    return kinds, q0, q1, ang
+
+
+def simulate(lib, n, gates, tile_bits, precision=0):
+    kinds, q0, q1, ang = arrays(gates)
+    out = np.zeros(2 << n, np.float64)
+    passes = lib.qvp_simulate(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data,
+                              ang.ctypes.data, precision, tile_bits, out.ctypes.data)
+    assert passes > 0
+    return out[0::2] + 1j * out[1::2], passes
+
+
+def stats(lib, n, gates, tile_bits=0, precision=0):
+    kinds, q0, q1, _ = arrays(gates)
+    st = np.zeros(6, np.int64)
+    pm = np.zeros(256, np.int32)
+    assert lib.qvp_plan_stats(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data,
+                              precision, tile_bits, st.ctypes.data, pm.ctypes.data, 256) == 0
+    return st, pm[: st[0]]
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_circuits_match_oracle_across_tile_sizes(plan_lib, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = int(rng.integers(1, 11))
+    gates = sv.random_circuit_gates(rng, n, int(rng.integers(0, 80)), extended=True)
+    want = sv.run_gates(n, gates)
+    for tile in (0, 5, 6, 8):
+        for precision in (0, 1):
+            if precision == 1 and tile == 5:
+                continue   # complex64 needs >= 6 tile bits (4 coalescing + 2)
+            got, _ = simulate(plan_lib, n, gates, tile, precision)
+            assert np.max(np.abs(got - want)) < 1e-12, (tile, precision)
+
+
+@pytest.mark.parametrize("n,layers,tile", [(8, 2, 5), (10, 2, 6), (12, 1, 7), (10, 3, 8)])
+def test_ddcl_layers_multi_pass(plan_lib, n, layers, tile):
+    tpl = sv.ddcl_template_gates(n, layers)
+    theta = sv.random_angles(6 * n * layers, 7)
+    gates = sv.bind_template(tpl, theta)
+    got, passes = simulate(plan_lib, n, gates, tile)
+    assert passes > 1
+    assert np.max(np.abs(got - sv.run_gates(n, gates))) < 1e-12
+
+
+def test_pass_counts_for_baseline_configs(plan_lib):
+    """Regression guard on the planner: HBM sweeps per circuit."""
+    expect_max = {(28, 8): 23, (20, 6): 11, (32, 4): 13}
+    for (n, layers), cap in expect_max.items():
+        gates = sv.bind_template(sv.ddcl_template_gates(n, layers), [0.1] * (6 * n * layers))
+        precision = 1 if n == 32 else 0
+        st, per_pass = stats(plan_lib, n, gates, 0, precision)
+        assert st[5] == 0 and st[0] <= cap, (n, layers, st)
+        assert per_pass.sum() == st[2]
+
+
+def test_small_register_is_single_tile(plan_lib):
+    gates = sv.bind_template(sv.ddcl_template_gates(4, 2), [0.3] * 48)
+    st, _ = stats(plan_lib, 4, gates)
+    assert st[5] == 1 and st[0] == 1 and st[4] == 4
