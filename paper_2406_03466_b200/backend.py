@@ -217,7 +217,12 @@ class B200Backend:
         if ok:
             if config.mode != "expectation":
                 raise ExecutionError(ok[0].name, "counts mode is not implemented by the B200 backend")
-            buffer.extend_children(self._children(ok, n))
+            children = self._children(ok, n)
+            if hasattr(buffer, "extend_children"):
+                buffer.extend_children(children)
+            else:   # a reference `qvirt.ResultBuffer`
+                for child in children:
+                    buffer.append_child(child)
         if stop < len(circuits):
             raise ExecutionError(circuits[stop].name, reason)
 
@@ -276,15 +281,15 @@ class B200Backend:
         xs, ys, zs, coeffs, consts = [], [], [], [], []
         for c in circuits:
             obs = c.observable
-            terms = (obs,) if isinstance(obs, PauliTerm) else obs.terms
-            for t in terms:
+            single = not hasattr(obs, "terms")   # a PauliTerm (ours or the reference's)
+            for t in ((obs,) if single else obs.terms):
                 xm, ym, zm = term_masks(t, n)
                 xs.append(xm)
                 ys.append(ym)
                 zs.append(zm)
                 coeffs.append(t.coefficient)
             offsets.append(len(xs))
-            consts.append(None if isinstance(obs, PauliTerm) else obs.constant)
+            consts.append(None if single else obs.constant)
         lowered = lower_batch(circuits)
         vals = self._run(lowered, n, native.QV_OUT_PAULI, circuits,
                          terms=(np.asarray(offsets, np.int64), np.asarray(xs, np.uint64),

@@ -1,0 +1,171 @@
+"""Parity of the B200 executor with the reference, on the GPU.
+
+Golden vectors come from the reference implementation (tests/golden/);
+tolerances are the north star's: 1e-10 absolute for complex128 states,
+1e-5 for complex64.  Everything goes through the public API and the C ABI.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2406_03466_b200 as qv
+from oracle import statevector as sv
+
+pytestmark = pytest.mark.gpu
+
+TOL128 = 1e-10
+TOL64 = 1e-5
+
+
+def circuit_from_case(case, name="c"):
+    gates = tuple(qv.Gate(qv.GateKind(k), tuple(t), a) for k, t, a in case["gates"])
+    return qv.Circuit(case["n"], gates, name=name)
+
+
+def observable_from_case(case):
+    obs = case["observable"]
+    terms = [qv.PauliTerm(tuple(tuple(f) for f in factors), c) for factors, c in obs["terms"]]
+    if obs["constant"] is None:
+        return terms[0]
+    return qv.Observable(tuple(terms), obs["constant"])
+
+
+def test_random_circuit_expectations(gpu, golden_small):
+    backend = qv.B200Backend(device=0)
+    for case in golden_small["random_circuits"]:
+        c = circuit_from_case(case).with_observable(observable_from_case(case))
+        buf = qv.ResultBuffer(n_qubits=case["n"])
+        backend.execute(buf, [c], qv.ExecutionConfig())
+        assert buf.children[0].expectation == pytest.approx(case["expectation"], abs=TOL128), case["n"]
+
+
+def test_random_circuit_distributions(gpu, golden_small):
+    backend = qv.B200Backend(device=0)
+    for case in golden_small["random_circuits"]:
+        if "distribution" not in case:
+            continue
+        buf = qv.ResultBuffer(n_qubits=case["n"])
+        backend.execute(buf, [circuit_from_case(case)], qv.ExecutionConfig())
+        got, want = buf.children[0].distribution, case["distribution"]
+        keys = set(got) | set(want)
+        assert max(abs(got.get(k, 0.0) - want.get(k, 0.0)) for k in keys) < TOL128
+
+
+def test_qcl_config1_gradients(gpu, golden_small):
+    """Config 1: QCL 4 qubits x 2 layers, 64 synthetic points."""
+    cfg = golden_small["qcl_config1"]
+    n, layers = cfg["n"], cfg["layers"]
+    worst = 0.0
+    for pt in cfg["points"]:
+        theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), pt["theta_seed"])
+        target = qv.random_target_distribution(n, pt["target_seed"])
+        rep = qv.ddcl_gradient(qv.DdclSpec(n, layers, theta, target), qv.VqpuPoolConfig())
+        worst = max(worst, float(np.max(np.abs(np.array(rep.gradient) - pt["gradient"]))))
+        assert rep.n_circuit_executions == 2 * len(theta)
+    assert worst < TOL128
+
+
+def test_qcl_children_path_matches_losses(gpu, golden_small):
+    """Through execute_parallel + ChildResult distributions (support +
+    remainder), the reference's own JS on the children reproduces the losses."""
+    cfg = golden_small["qcl_config1"]
+    n, layers = cfg["n"], cfg["layers"]
+    pt = cfg["points"][3]
+    theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), pt["theta_seed"])
+    target = qv.random_target_distribution(n, pt["target_seed"])
+    buf = qv.ResultBuffer(n_qubits=n)
+    rep = qv.ddcl_gradient(qv.DdclSpec(n, layers, theta, target), qv.VqpuPoolConfig(n_virtual_qpus=3), buffer=buf)
+    losses = [qv.js_divergence(target, c.distribution) for c in buf.children]
+    assert np.max(np.abs(np.array(losses) - pt["losses"])) < TOL128
+    assert np.max(np.abs(np.array(rep.gradient) - pt["gradient"])) < TOL128
+    assert buf.child_names()[:2] == ["k0+", "k0-"]
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_mcvqe_gradients(gpu, golden_small, idx):
+    case = golden_small["mcvqe"][idx]
+    n = case["n"]
+    ham = qv.aiem_hamiltonian(qv.random_aiem_coefficients(n, case["coeff_seed"]))
+    spec = qv.McvqeAnsatzSpec(qv.random_cis_amplitudes(n, case["cis_seed"]),
+                              qv.random_angles(qv.mcvqe_parameter_count(n), case["theta_seed"]))
+    rep = qv.mcvqe_gradient(ham, spec, qv.VqpuPoolConfig())
+    assert rep.n_circuit_executions == case["n_circuits"]
+    assert np.max(np.abs(np.array(rep.gradient) - case["gradient"])) < TOL128
+    buf = qv.ResultBuffer(n_qubits=n)
+    rep2 = qv.mcvqe_gradient(ham, spec, qv.VqpuPoolConfig(n_virtual_qpus=4), buffer=buf)
+    vals = np.array([c.expectation for c in buf.children])
+    assert np.max(np.abs(vals - case["values"])) < TOL128
+    assert buf.child_names()[: len(case["names"])] == case["names"]
+    assert np.max(np.abs(np.array(rep2.gradient) - case["gradient"])) < TOL128
+    assert qv.mcvqe_energy(ham, spec) == pytest.approx(case["energy"], abs=TOL128)
+
+
+def test_qcl_forward_and_shifted_losses(gpu, golden_large):
+    backend = qv.B200Backend(device=0)
+    for case in golden_large["qcl_forward"]:
+        n, layers = case["n"], case["layers"]
+        theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), case["theta_seed"])
+        target = qv.random_target_distribution(n, case["target_seed"])
+        spec = qv.DdclSpec(n, layers, theta, target)
+        js = backend.js_losses([qv.ddcl_circuit(spec)], n, target)[0]
+        assert js == pytest.approx(case["js"], abs=TOL128), n
+        if case["shifted"]:
+            batch = qv.ddcl_batch(spec)
+            pick = [2 * s["k"] + (0 if s["tag"] == "+" else 1) for s in case["shifted"]]
+            got = backend.js_losses([batch[i] for i in pick], n, target)
+            assert np.max(np.abs(got - [s["js"] for s in case["shifted"]])) < TOL128, n
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_qcl_full_gradient_multi_tile(gpu, golden_large, idx):
+    """Whole shifted batch through the prefix-sharing scheduler (14q: state
+    in HBM, several passes per circuit)."""
+    case = golden_large["qcl_gradient"][idx]
+    n, layers = case["n"], case["layers"]
+    theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), case["theta_seed"])
+    target = qv.random_target_distribution(n, case["target_seed"])
+    spec = qv.DdclSpec(n, layers, theta, target)
+    backend = qv.B200Backend(device=0)
+    losses = backend.js_losses(qv.ddcl_batch(spec), n, target)
+    assert np.max(np.abs(losses - case["losses"])) < TOL128
+    rep = qv.ddcl_gradient(spec, qv.VqpuPoolConfig(n_virtual_qpus=5))
+    assert np.max(np.abs(np.array(rep.gradient) - case["gradient"])) < TOL128
+
+
+def test_complex64_within_1e5(gpu, golden_small, golden_large):
+    cfg = golden_small["qcl_config1"]
+    n, layers = cfg["n"], cfg["layers"]
+    pt = cfg["points"][0]
+    theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), pt["theta_seed"])
+    target = qv.random_target_distribution(n, pt["target_seed"])
+    rep = qv.ddcl_gradient(qv.DdclSpec(n, layers, theta, target), qv.VqpuPoolConfig(),
+                           backend_factory=lambda: qv.B200Backend(precision="complex64", support=target))
+    # children path (custom factory) in complex64
+    assert np.max(np.abs(np.array(rep.gradient) - pt["gradient"])) < TOL64
+    backend = qv.B200Backend(device=0, precision="complex64")
+    for case in golden_large["qcl_forward"]:
+        n, layers = case["n"], case["layers"]
+        theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), case["theta_seed"])
+        target = qv.random_target_distribution(n, case["target_seed"])
+        js = backend.js_losses([qv.ddcl_circuit(qv.DdclSpec(n, layers, theta, target))], n, target)[0]
+        assert js == pytest.approx(case["js"], abs=TOL64), n
+    mc = golden_small["mcvqe"][0]
+    ham = qv.aiem_hamiltonian(qv.random_aiem_coefficients(8, mc["coeff_seed"]))
+    spec = qv.McvqeAnsatzSpec(qv.random_cis_amplitudes(8, mc["cis_seed"]), qv.random_angles(36, mc["theta_seed"]))
+    vals = backend.expectation_values(qv.mcvqe_gradient_batch(ham, spec), 8)
+    assert np.max(np.abs(vals - mc["values"])) < TOL64
+
+
+def test_extension_gates_rx_cz_against_oracle(gpu):
+    backend = qv.B200Backend(device=0)
+    for seed, n in ((1, 3), (2, 7), (3, 13), (4, 15)):
+        rng = np.random.Generator(np.random.PCG64(seed))
+        gates = sv.random_circuit_gates(rng, n, 150, extended=True)
+        circ = qv.Circuit(n, tuple(qv.Gate(qv.GateKind(k), t, a) for k, t, a in gates), name="e")
+        term = qv.pauli({0: "Y", n - 1: "X"}, 0.7)
+        got = backend.expectation_values([circ.with_observable(term)], n)[0]
+        amps = sv.run_gates(n, gates)
+        want = 0.7 * sv.pauli_expectation(amps, n, *sv.term_masks(term.factors, n))
+        assert got == pytest.approx(want, abs=TOL128), n
