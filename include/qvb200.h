@@ -130,7 +130,9 @@ int64_t qv_last_error_circuit(qv_handle handle);
  * [2] sweeps a schedule without prefix sharing would run, [3] unique states simulated,
  * [4] algorithmic HBM bytes moved by pass kernels, [5] device ms of pass kernels
  * (CUDA events on the executor stream), [6] passes per circuit, [7] tile bits k,
- * [8] total device ms of the call. */
+ * [8] device ms of the call (first to last kernel), [9] host->device bytes,
+ * [10] device->host bytes, [11] algorithmic flops of pass kernels
+ * (28 per amplitude pair per fused 2x2 matrix). */
 int qv_last_stats(qv_handle handle, double* stats, int32_t n_stats);
 
 /* Library version string, e.g. "qvb200 0.1 sm_100a". */

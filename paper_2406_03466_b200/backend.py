@@ -247,7 +247,7 @@ class B200Backend:
         return out
 
     # -- internals -----------------------------------------------------------
-    def _precheck(self, c, n: int) -> str:
+    def _precheck(self, c, n: int, children: bool = True) -> str:
         if c.n_qubits != n:
             return f"circuit has {c.n_qubits} qubits, buffer {n}"
         if c.is_parameterized:
@@ -256,14 +256,14 @@ class B200Backend:
         obs = c.observable
         if obs is not None and obs.min_qubits > n:
             return f"term on qubit {obs.min_qubits - 1} exceeds {n} qubits"
-        if obs is None and self._support_spec is None and n > MAX_FULL_DISTRIBUTION_QUBITS:
+        if children and obs is None and self._support_spec is None and n > MAX_FULL_DISTRIBUTION_QUBITS:
             return (f"a full {n}-qubit distribution has 2^{n} entries; construct the backend "
                     "with support= to receive the target support plus the remainder")
         return ""
 
     def _check_all(self, circuits, n):
         for c in circuits:
-            reason = self._precheck(c, n)
+            reason = self._precheck(c, n, children=False)
             if reason:
                 raise ExecutionError(c.name, reason)
 

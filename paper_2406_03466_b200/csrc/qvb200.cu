@@ -121,6 +121,17 @@ struct Engine {
     }
 };
 
+// Host<->device copies of a call, counted for the e2e byte figures (stats[9], [10]).
+inline void h2d(Engine& E, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, E.stream));
+    E.stats[9] += (double)bytes;
+}
+inline void d2h(Engine& E, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, E.stream));
+    CK(cudaStreamSynchronize(E.stream));
+    E.stats[10] += (double)bytes;
+}
+
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -243,19 +254,24 @@ struct GroupRun {
 
 template <typename T>
 void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const LaunchEntry* d_ent, int nstates,
-                 int64_t ntiles, const EpiArgs& ep, bool timed) {
+                 int64_t ntiles, const EpiArgs& ep, bool generated) {
     typedef typename Cx<T>::V V;
     constexpr int NT = sizeof(T) == 8 ? kNT128 : kNT64;
     const size_t smem = (sizeof(V) << pd.k) + (size_t)pd.ng * sizeof(GroupDesc) + (size_t)pd.nm * 8 * sizeof(T) + 32 * sizeof(double);
     const int threads = std::max(32, 1 << (pd.k - kRegBits));
     const int64_t blocks = ntiles * nstates;
     if (blocks > 0x7fffffffll) throw ArgError("launch too large");
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (timed) { e0 = E.next_event(); e1 = E.next_event(); CK(cudaEventRecord(e0, E.stream)); }
+    cudaEvent_t e0 = E.next_event(), e1 = E.next_event();
+    CK(cudaEventRecord(e0, E.stream));
     pass_kernel<T, NT><<<(unsigned)blocks, threads, smem, E.stream>>>(pd, d_groups, d_ent, nstates, ep);
     CK(cudaGetLastError());
-    if (timed) { CK(cudaEventRecord(e1, E.stream)); E.timed.push_back({e0, e1}); }
+    CK(cudaEventRecord(e1, E.stream));
+    E.timed.push_back({e0, e1});
     E.stats[0] += 1;
+    // algorithmic FP64/FP32 work: 2^(n-1) pairs x 28 flops per fused 2x2
+    // matrix (a |0> input only computes tile 0 of a multi-tile state)
+    const double amps = (generated && ntiles > 1) ? (double)(1ll << pd.k) : std::ldexp(1.0, ep.n);
+    E.stats[11] += (double)nstates * amps * 14.0 * pd.nm;
 }
 
 template <typename T>
@@ -301,7 +317,7 @@ void GroupRun::run() {
         for (size_t j = 0; j < slots8; ++j) umats[(size_t)u * slots8 + j] = (T)src[j];
     }
     T* d_mats = reinterpret_cast<T*>(E.d_mats.get(std::max<size_t>(1, umats.size()) * sizeof(T)));
-    if (!umats.empty()) CK(cudaMemcpyAsync(d_mats, umats.data(), umats.size() * sizeof(T), cudaMemcpyHostToDevice, E.stream));
+    if (!umats.empty()) h2d(E, d_mats, umats.data(), umats.size() * sizeof(T));
 
     // 4. result plumbing per unique state
     EpiArgs ep;
@@ -332,10 +348,10 @@ void GroupRun::run() {
         uint64_t* dph = E.d_tphase.get(NTm);
         int64_t* dto = E.d_term_off.get(U + 1);
         if (NTm) {
-            CK(cudaMemcpyAsync(dfl, fl.data(), NTm * 8, cudaMemcpyHostToDevice, E.stream));
-            CK(cudaMemcpyAsync(dph, ph.data(), NTm * 8, cudaMemcpyHostToDevice, E.stream));
+            h2d(E, dfl, fl.data(), NTm * 8);
+            h2d(E, dph, ph.data(), NTm * 8);
         }
-        CK(cudaMemcpyAsync(dto, term_off_u.data(), (U + 1) * 8, cudaMemcpyHostToDevice, E.stream));
+        h2d(E, dto, term_off_u.data(), (U + 1) * 8);
         ep.term_off = dto;
         ep.t_flip = dfl;
         ep.t_phase = dph;
@@ -343,11 +359,11 @@ void GroupRun::run() {
     }
     if (ep.S > 0) {
         uint64_t* dsu = E.d_support.get(ep.S);
-        CK(cudaMemcpyAsync(dsu, R->support, ep.S * 8, cudaMemcpyHostToDevice, E.stream));
+        h2d(E, dsu, R->support, ep.S * 8);
         ep.support = dsu;
         if (R->kind == QV_OUT_JS) {
             double* dta = E.d_target.get(ep.S);
-            CK(cudaMemcpyAsync(dta, R->target, ep.S * 8, cudaMemcpyHostToDevice, E.stream));
+            h2d(E, dta, R->target, ep.S * 8);
             ep.target = dta;
         }
     }
@@ -364,7 +380,7 @@ void GroupRun::run() {
         std::vector<LaunchEntry> ents(U);
         for (int64_t u = 0; u < U; ++u) ents[u] = {nullptr, nullptr, d_mats + (size_t)u * slots8, u, 0, 0};
         LaunchEntry* dent = E.d_entries.get(U);
-        CK(cudaMemcpyAsync(dent, ents.data(), U * sizeof(LaunchEntry), cudaMemcpyHostToDevice, E.stream));
+        h2d(E, dent, ents.data(), U * sizeof(LaunchEntry));
         ep.flags = F_SINGLE;
         if (R->kind == QV_OUT_PAULI) ep.flags |= F_S_PAULI;
         if (R->kind == QV_OUT_SUPPORT) ep.flags |= F_S_SUPPORT;
@@ -372,7 +388,7 @@ void GroupRun::run() {
         if (R->kind == QV_OUT_FULL) ep.flags |= F_S_FULL;
         ep.ntiles = 1;
         if (U > 0x7fffffffll) throw ArgError("batch too large");
-        launch_pass<T>(E, plan.pdesc[0], cp.d_groups.p, dent, (int)U, 1, ep, true);
+        launch_pass<T>(E, plan.pdesc[0], cp.d_groups.p, dent, (int)U, 1, ep, false);
         E.stats[1] += (double)U;
         E.stats[2] += (double)C;
     } else {
@@ -408,9 +424,9 @@ void GroupRun::run() {
             int32_t* doff = E.d_sup_off.get(ntiles + 1);
             int32_t* dloc = E.d_sup_local.get(ep.S);
             int32_t* dpos = E.d_sup_pos.get(ep.S);
-            CK(cudaMemcpyAsync(doff, cnt.data(), (ntiles + 1) * 4, cudaMemcpyHostToDevice, E.stream));
-            CK(cudaMemcpyAsync(dloc, sl.data(), ep.S * 4, cudaMemcpyHostToDevice, E.stream));
-            CK(cudaMemcpyAsync(dpos, sp.data(), ep.S * 4, cudaMemcpyHostToDevice, E.stream));
+            h2d(E, doff, cnt.data(), (ntiles + 1) * 4);
+            h2d(E, dloc, sl.data(), ep.S * 4);
+            h2d(E, dpos, sp.data(), ep.S * 4);
             ep.sup_off = doff;
             ep.sup_local = dloc;
             ep.sup_pos = dpos;
@@ -529,17 +545,17 @@ void GroupRun::run() {
 
         // ---- upload tables once, then issue every launch -----------------
         LaunchEntry* dent = E.d_entries.get(ents.size());
-        CK(cudaMemcpyAsync(dent, ents.data(), ents.size() * sizeof(LaunchEntry), cudaMemcpyHostToDevice, E.stream));
+        h2d(E, dent, ents.data(), ents.size() * sizeof(LaunchEntry));
         int64_t* dslots = E.d_slots.get(std::max<size_t>(2, slots_tab.size()));
         if (!slots_tab.empty())
-            CK(cudaMemcpyAsync(dslots, slots_tab.data(), slots_tab.size() * 8, cudaMemcpyHostToDevice, E.stream));
+            h2d(E, dslots, slots_tab.data(), slots_tab.size() * 8);
         for (const L& l : sched) {
             if (l.kind == L_PASS) {
                 EpiArgs e2 = ep;
                 e2.flags = l.flags;
                 e2.partial = partial;
                 if (!(l.flags & F_SUPPORT)) e2.sup_off = nullptr;
-                launch_pass<T>(E, plan.pdesc[l.pass], cp.d_groups.p, dent + l.off, l.count, ntiles, e2, true);
+                launch_pass<T>(E, plan.pdesc[l.pass], cp.d_groups.p, dent + l.off, l.count, ntiles, e2, l.pass == 0);
                 E.stats[1] += l.count;
                 E.stats[4] += l.bytes;
             } else if (l.kind == L_FINAL_DIST) {
@@ -579,22 +595,22 @@ void GroupRun::run() {
     E.stats[8] += call_ms;
     if (R->kind == QV_OUT_PAULI) {
         std::vector<double> vals(uterm_src.size());
-        if (!vals.empty()) CK(cudaMemcpy(vals.data(), ep.pauli_out, vals.size() * 8, cudaMemcpyDeviceToHost));
+        if (!vals.empty()) d2h(E, vals.data(), ep.pauli_out, vals.size() * 8);
         for (size_t j = 0; j < uterm_src.size(); ++j) out[uterm_src[j]] = vals[j];
     } else if (R->kind == QV_OUT_SUPPORT) {
         const size_t row = (size_t)ep.S + 1;
         std::vector<double> vals((size_t)U * row);
-        CK(cudaMemcpy(vals.data(), ep.sup_out, vals.size() * 8, cudaMemcpyDeviceToHost));
+        d2h(E, vals.data(), ep.sup_out, vals.size() * 8);
         for (int64_t i = 0; i < C; ++i)
             std::memcpy(out + (size_t)circuits[i] * row, vals.data() + (size_t)uniq_of[i] * row, row * 8);
     } else if (R->kind == QV_OUT_JS) {
         std::vector<double> vals(U);
-        CK(cudaMemcpy(vals.data(), ep.js_out, U * 8, cudaMemcpyDeviceToHost));
+        d2h(E, vals.data(), ep.js_out, U * 8);
         for (int64_t i = 0; i < C; ++i) out[circuits[i]] = vals[uniq_of[i]];
     } else {
         const size_t row = (size_t)1 << n;
         std::vector<double> vals((size_t)U * row);
-        CK(cudaMemcpy(vals.data(), ep.full_out, vals.size() * 8, cudaMemcpyDeviceToHost));
+        d2h(E, vals.data(), ep.full_out, vals.size() * 8);
         for (int64_t i = 0; i < C; ++i)
             std::memcpy(out + (size_t)circuits[i] * row, vals.data() + (size_t)uniq_of[i] * row, row * 8);
     }

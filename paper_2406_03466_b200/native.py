@@ -27,7 +27,8 @@ EXPORTS = ("qv_version", "qv_output_size", "qv_create", "qv_destroy", "qv_execut
            "qv_last_error", "qv_last_error_circuit", "qv_last_stats", "qv_device_count")
 
 STAT_NAMES = ("launches", "sweeps", "sweeps_unshared", "unique_states", "pass_bytes",
-              "pass_ms", "passes_per_circuit", "tile_bits", "device_ms")
+              "pass_ms", "passes_per_circuit", "tile_bits", "device_ms", "h2d_bytes", "d2h_bytes",
+              "pass_flops")
 
 
 class NativeUnavailable(RuntimeError):
