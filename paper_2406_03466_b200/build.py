@@ -53,6 +53,17 @@ def build_product(force: bool = False, verbose_ptxas: bool = False) -> Path:
     return PRODUCT
 
 
+TRACE = PKG / "libqvb200_trace.so"
+
+
+def build_trace(force: bool = False) -> Path:
+    """Debug build with per-phase clock64() tracing (tools/trace_pass.py)."""
+    if force or _stale(TRACE, PRODUCT_DEPS):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-DQV_TRACE",
+              "-cudart", "static", f"-I{INCLUDE}", f"-I{CSRC}", "-o", TRACE, *PRODUCT_SOURCES])
+    return TRACE
+
+
 def build_plancheck(force: bool = False) -> Path:
     if force or _stale(PLANCHECK, PLANCHECK_DEPS):
         _run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", f"-I{CSRC}", "-o", PLANCHECK, *PLANCHECK_SOURCES])

@@ -1,17 +1,19 @@
 // kernels.cuh — sm_100a state-vector kernels.
 //
-// pass_kernel: one HBM sweep of a plan pass over a batch of states.  A CTA
-//   owns one tile (2^k amplitudes spread over the pass's k index bits), stages
-//   it in shared memory with 128-bit coalesced loads, applies the pass's
-//   register groups (16 amplitudes per thread, up to four fused 2x2 matrices
-//   per group, CNOTs folded into the slot map at plan time so they cost no
-//   data movement), and writes the tile back -- or, on a state's last pass,
-//   reduces it (norm, support probabilities, Pauli terms, JS loss) without
-//   writing it.  Replaces the per-gate full sweeps of the reference
-//   (pkg/src/qvirt/kernels.py:18-70) and its reductions (:73-94).
+// pass_kernel: one HBM sweep of a plan pass over a batch of states.  CTAs are
+//   persistent per state: a CTA stages the pass's group descriptors and its
+//   state's fused matrices once, then walks tiles (2^k amplitudes spread over
+//   the pass's k index bits).  Per tile it stages the amplitudes in shared
+//   memory with 128-bit coalesced loads, applies the register groups (16
+//   amplitudes per thread, up to four fused 2x2 matrices per group; CNOTs were
+//   folded into the slot maps at plan time so they move no data), and writes
+//   the tile back -- or, on a state's last pass, reduces it (norm, support
+//   probabilities, Pauli terms, JS loss) without writing it.  Replaces the
+//   per-gate full sweeps of the reference (pkg/src/qvirt/kernels.py:18-70) and
+//   its reductions (:73-94).
 //
 // All reductions are fixed-shape trees in FP64 with no atomics, so a result
-// depends only on the circuit, never on its position in a launch or on the GPU.
+// depends only on the circuit, never on its position in a launch or the GPU.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -45,7 +47,7 @@ struct EpiArgs {
     int flags;
     int n;
     int64_t ntiles;
-    double* partial;           // [rslot * ntiles + tile]
+    double* partial;           // [pslot * ntiles + tile]
     const int32_t* sup_off;    // multi-tile support CSR over tiles [ntiles + 1]
     const int32_t* sup_local;
     const int32_t* sup_pos;
@@ -59,21 +61,35 @@ struct EpiArgs {
     const uint64_t* t_flip;
     const uint64_t* t_phase;
     double* pauli_out;         // [term]
+    long long* trace;          // QV_TRACE builds only: per-phase clock64() of CTA 0
 };
+
+#ifdef QV_TRACE
+// trace[(item * 64 + event) * 16 + warp]: event 0 item start, 1 tile resident,
+// 2 + 2g group g math done, 3 + 2g group g synchronised, 62 store done
+#define QV_MARK(ev)                                                                                \
+    do {                                                                                           \
+        if (ep.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && i < 8 && (threadIdx.x >> 5) < 16) \
+            ep.trace[((i) * 64 + (ev)) * 16 + (threadIdx.x >> 5)] = clock64();                     \
+    } while (0)
+#else
+#define QV_MARK(ev) \
+    do {            \
+    } while (0)
+#endif
 
 template <typename T> struct Cx;
 template <> struct Cx<double> { typedef double2 V; };
 template <> struct Cx<float> { typedef float2 V; };
 
-template <typename T, typename V>
-__device__ __forceinline__ void rot2(const T* __restrict__ m, V& u, V& v) {
-    const T m00r = m[0], m00i = m[1], m01r = m[2], m01i = m[3];
-    const T m10r = m[4], m10i = m[5], m11r = m[6], m11i = m[7];
+// (u, v) <- [[m00, m01], [m10, m11]] (u, v); 4 multiplies + 12 FMAs per pair.
+template <typename V>
+__device__ __forceinline__ void rot2(const V m00, const V m01, const V m10, const V m11, V& u, V& v) {
     V a, b;
-    a.x = fma(m00r, u.x, fma(-m00i, u.y, fma(m01r, v.x, -m01i * v.y)));
-    a.y = fma(m00r, u.y, fma(m00i, u.x, fma(m01r, v.y, m01i * v.x)));
-    b.x = fma(m10r, u.x, fma(-m10i, u.y, fma(m11r, v.x, -m11i * v.y)));
-    b.y = fma(m10r, u.y, fma(m10i, u.x, fma(m11r, v.y, m11i * v.x)));
+    a.x = fma(m00.x, u.x, fma(-m00.y, u.y, fma(m01.x, v.x, -m01.y * v.y)));
+    a.y = fma(m00.x, u.y, fma(m00.y, u.x, fma(m01.x, v.y, m01.y * v.x)));
+    b.x = fma(m10.x, u.x, fma(-m10.y, u.y, fma(m11.x, v.x, -m11.y * v.y)));
+    b.y = fma(m10.x, u.y, fma(m10.y, u.x, fma(m11.x, v.y, m11.y * v.x)));
     u = a;
     v = b;
 }
@@ -102,192 +118,255 @@ __device__ __forceinline__ double js_term(double p, double q) {
     return r;
 }
 
-template <typename T, int NT>
-__global__ void __launch_bounds__(NT, 2) pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc,
-                                                  const LaunchEntry* __restrict__ ent, int nstates, EpiArgs ep) {
+template <typename V>
+__device__ __forceinline__ double norm2(const V v) {
+    return (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+}
+
+__host__ __device__ constexpr int pass_threads(int tb) { return tb >= 5 ? (1 << tb) : 32; }
+
+// Ampere-style async global->shared copies (LDGSTS): the next tile streams in
+// while the current one is computed.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// TB = tile bits - 4 = log2(active threads).  Work items are (state, tile)
+// pairs, state fastest: item w = tile * nstates + state.  Persistent CTA c
+// takes items c, c + G, c + 2G, ... (G = grid size = one full wave), so CTAs
+// running at the same time touch the same tile of different states -- a
+// shared trunk input is then read once from HBM and reused from L2.
+//
+// DB (double buffer): two tile buffers; the next item's tile streams in with
+// cp.async while the current one is computed and written back, so HBM, the
+// shared-memory pipe and the FP64 pipe work concurrently inside one CTA.
+template <typename T, int TB, bool DB>
+__global__ void __launch_bounds__(pass_threads(TB), (DB || TB >= 9 ? 1 : TB == 8 ? 2 : 4))
+pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent,
+            int nstates, int unused, EpiArgs ep) {
     typedef typename Cx<T>::V V;
+    constexpr int NT = 1 << TB;             // active threads (TB < 5: a partial warp)
+    constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);   // register bits per group
+    constexpr int NA = 1 << R;                           // amplitudes per thread
+    constexpr int K = TB + R;
+    constexpr size_t TILE = sizeof(V) << K;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int k = pd.k;
-    const int tb = k - kRegBits;          // thread bits
-    const int nt = 1 << tb;               // active threads
-    V* tile = reinterpret_cast<V*>(smem_raw);
-    GroupDesc* sg = reinterpret_cast<GroupDesc*>(smem_raw + (sizeof(V) << k));
-    T* smat = reinterpret_cast<T*>(sg + pd.ng);
-    double* sred = reinterpret_cast<double*>(smat + (size_t)pd.nm * 8);
+    GroupDesc* sg = reinterpret_cast<GroupDesc*>(smem_raw + TILE * (DB ? 2 : 1));
+    V* smat = reinterpret_cast<V*>(sg + pd.ng);                            // 4 complex per matrix
+    double* sred = reinterpret_cast<double*>(smat + (size_t)pd.nm * 4);
+    (void)unused;
 
     const int tid = threadIdx.x;
-    const int64_t bid = blockIdx.x;
-    const int y = (int)(bid % nstates);
-    const int64_t x = bid / nstates;
-    const LaunchEntry e = ent[y];
-
-    {   // stage groups and this state's matrices
-        const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(gdesc + pd.g0);
-        uint32_t* gdst = reinterpret_cast<uint32_t*>(sg);
-        for (int i = tid; i < pd.ng * 16; i += blockDim.x) gdst[i] = gsrc[i];
-        const T* msrc = reinterpret_cast<const T*>(e.mats) + (size_t)pd.m0 * 8;
-        for (int i = tid; i < pd.nm * 8; i += blockDim.x) smat[i] = msrc[i];
+    const int64_t ntiles = ep.ntiles;
+    const int64_t items = ntiles * nstates;
+    const int64_t G = gridDim.x;
+    {   // stage the pass's group descriptors (once per CTA)
+        const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
+        uint4* gdst = reinterpret_cast<uint4*>(sg);
+        for (int i = tid; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
     }
-    uint64_t outer = 0;
-    for (int j = 0; j < pd.n_outer; ++j)
-        if ((x >> j) & 1) outer |= 1ull << pd.obits[j];
-
-    const bool active = tid < nt;
-    uint32_t tslot = 0;
+    const bool active = tid < NT;
+    // per-thread parts of the load / store maps (tile-independent)
+    uint32_t tslot = 0, fslot = 0;
     uint64_t tg = 0;
-    for (int j = 0; j < tb; ++j)
-        if ((tid >> j) & 1) { tslot ^= pd.swz[j]; tg |= 1ull << pd.sbits[j]; }
-    const bool gen = e.in == nullptr;
-    const bool zero_tile = gen && x != 0;
-    if (active) {
-        if (gen) {
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                V v;
-                v.x = (x == 0 && tid == 0 && it == 0) ? T(1) : T(0);
-                v.y = T(0);
-                tile[tslot ^ pd.swz_hi[it]] = v;
-            }
-        } else {
-            const V* __restrict__ in = reinterpret_cast<const V*>(e.in);
-            V r[16];
+    for (int j = 0; j < TB; ++j)
+        if ((tid >> j) & 1) { tslot ^= pd.swz[j]; fslot ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
+    auto outer_of = [&](int64_t x) {
+        uint64_t o = 0;
+        for (int j = 0; j < pd.n_outer; ++j)
+            if ((x >> j) & 1) o |= 1ull << pd.obits[j];
+        return o;
+    };
+    auto issue_load = [&](int64_t w, unsigned char* dst) {   // NA async 8/16-byte copies per thread
+        const V* in = reinterpret_cast<const V*>(ent[w % nstates].in);
+        if (in == nullptr || !active) return;
+        const V* src = in + (outer_of(w / nstates) | tg);
 #pragma unroll
-            for (int it = 0; it < 16; ++it) r[it] = __ldcs(in + (outer | tg | pd.g_hi[it]));
-#pragma unroll
-            for (int it = 0; it < 16; ++it) tile[tslot ^ pd.swz_hi[it]] = r[it];
-        }
-    }
-    __syncthreads();
+        for (int it = 0; it < NA; ++it)
+            cp_async<sizeof(V)>(dst + (size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V), src + pd.g_hi[it]);
+    };
+    if (blockIdx.x < items) issue_load(blockIdx.x, smem_raw);
+    cp_async_commit();
 
-    if (!zero_tile) {
-        for (int g = 0; g < pd.ng; ++g) {
-            if (active) {
-                const GroupDesc& G = sg[g];
-                uint32_t base = 0;
-                for (int m = 0; m < tb; ++m)
-                    if ((tid >> m) & 1) base ^= G.tcol[m];
-                V a[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) a[j] = tile[base ^ G.combo[j]];
-#pragma unroll
-                for (int r = 0; r < kRegBits; ++r) {
-                    const int mi = G.mat[r];
-                    if (mi >= 0) {
-                        const T* M = smat + mi * 8;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (!((j >> r) & 1)) rot2<T, V>(M, a[j], a[j | (1 << r)]);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 16; ++j) tile[base ^ G.combo[j]] = a[j];
-            }
-            __syncthreads();
+    int cur_y = -1;
+    LaunchEntry e;
+    int64_t i = 0;
+    for (int64_t w = blockIdx.x; w < items; w += G, ++i) {
+        const int y = (int)(w % nstates);
+        const int64_t x = w / nstates;
+        QV_MARK(0);
+        if (y != cur_y) {   // stage this state's matrices (the previous item is finished)
+            e = ent[y];
+            const V* msrc = reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4;
+            for (int q = tid; q < pd.nm * 4; q += blockDim.x) smat[q] = msrc[q];
+            cur_y = y;
         }
-    }
-
-    // ---- store / reduce -------------------------------------------------
-    uint32_t fslot = 0;
-    for (int j = 0; j < tb; ++j)
-        if ((tid >> j) & 1) fslot ^= pd.fin[j];
-    double acc = 0.0;
-    if (active) {
+        const bool gen = e.in == nullptr;
         V* __restrict__ out = reinterpret_cast<V*>(e.out);
         const bool store = (ep.flags & F_STORE) && out != nullptr;
-#pragma unroll
-        for (int it = 0; it < 16; ++it) {
-            const V v = tile[fslot ^ pd.fin_hi[it]];
-            if (store) __stcs(out + (outer | tg | pd.g_hi[it]), v);
-            acc += (double)v.x * (double)v.x + (double)v.y * (double)v.y;
-        }
-    }
-    if (!(ep.flags & (F_NORM | F_SINGLE | F_SUPPORT))) return;
-
-    if (ep.flags & F_NORM) {
-        const double s = block_sum(acc, sred);
-        if (tid == 0) ep.partial[e.pslot * ep.ntiles + x] = s;
-    }
-    if (ep.flags & F_SUPPORT) {
-        const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
-        double* row = ep.sup_out + e.rslot * (ep.S + 1);
-        for (int32_t i = lo + tid; i < hi; i += blockDim.x) {
-            const uint32_t slot = apply_cols(pd.fin, k, (uint32_t)ep.sup_local[i]);
-            const V v = tile[slot];
-            row[ep.sup_pos[i]] = (double)v.x * (double)v.x + (double)v.y * (double)v.y;
-        }
-    }
-    if (!(ep.flags & F_SINGLE)) return;
-
-    // ---- single-tile epilogue: the tile is the whole state ----------------
-    const double total = block_sum(acc, sred);
-    const int64_t dim = 1ll << ep.n;
-    if (ep.flags & F_S_FULL) {
-        double* row = ep.full_out + (e.rslot << ep.n);
-        if (active) {
-#pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                const uint32_t i = (uint32_t)tid | ((uint32_t)it << tb);
-                if (i < dim) {
-                    const V v = tile[fslot ^ pd.fin_hi[it]];
-                    row[i] = ((double)v.x * (double)v.x + (double)v.y * (double)v.y) / total;
-                }
-            }
-        }
-    }
-    if (ep.flags & (F_S_SUPPORT | F_S_JS)) {
-        double* row = (ep.flags & F_S_SUPPORT) ? ep.sup_out + e.rslot * (ep.S + 1) : nullptr;
-        double jsum = 0.0, qsum = 0.0;
-        for (int64_t s = tid; s < ep.S; s += blockDim.x) {
-            const uint64_t idx = ep.support[s];
-            double q = 0.0;
-            if (idx < (uint64_t)dim) {
-                const V v = tile[apply_cols(pd.fin, k, (uint32_t)idx)];
-                q = ((double)v.x * (double)v.x + (double)v.y * (double)v.y) / total;
-            }
-            if (row) row[s] = q;
-            if (ep.flags & F_S_JS) { jsum += js_term(ep.target[s], q); qsum += q; }
-        }
-        if (row && tid == 0) row[ep.S] = total;
-        if (ep.flags & F_S_JS) {
-            const double J = block_sum(jsum, sred);
-            const double Q = block_sum(qsum, sred);
-            if (tid == 0) ep.js_out[e.rslot] = J + 0.5 * 0.69314718055994530942 * (1.0 - Q);
-        }
-    }
-    if (ep.flags & F_S_PAULI) {
-        const int64_t t0 = ep.term_off[e.rslot], t1 = ep.term_off[e.rslot + 1];
-        for (int64_t t = t0; t < t1; ++t) {
-            const uint64_t F = ep.t_flip[t], PH = ep.t_phase[t];
-            const uint32_t fF = apply_cols(pd.fin, k, (uint32_t)F);
-            double ar = 0.0, ai = 0.0;
+        unsigned char* tileb = smem_raw + ((DB && (i & 1)) ? TILE : 0);
+        const uint64_t outer = outer_of(x);
+        const bool zero_tile = gen && x != 0;
+        // ---- load (or generate |0...0>) ------------------------------------
+        if (gen) {
             if (active) {
 #pragma unroll
-                for (int it = 0; it < 16; ++it) {
-                    const uint32_t i = (uint32_t)tid | ((uint32_t)it << tb);
-                    const uint32_t sl = fslot ^ pd.fin_hi[it];
-                    const V a = tile[sl];
-                    const V b = tile[sl ^ fF];
-                    // conj(b) * a
-                    const double tr = (double)b.x * (double)a.x + (double)b.y * (double)a.y;
-                    const double ti = (double)b.x * (double)a.y - (double)b.y * (double)a.x;
-                    if (__popcll((uint64_t)i & PH) & 1) { ar -= tr; ai -= ti; }
-                    else { ar += tr; ai += ti; }
+                for (int it = 0; it < NA; ++it) {
+                    V v;
+                    v.x = (x == 0 && tid == 0 && it == 0) ? T(1) : T(0);
+                    v.y = T(0);
+                    *reinterpret_cast<V*>(tileb + ((size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V))) = v;
                 }
-            }
-            const double R = block_sum(ar, sred);
-            const double I = block_sum(ai, sred);
-            if (tid == 0) {
-                const int ny = __popcll(ep.t_flip[t] & ep.t_phase[t]) & 3;   // Y factors flip and carry phase
-                double val;
-                switch (ny) {
-                    case 0: val = R; break;
-                    case 1: val = -I; break;
-                    case 2: val = -R; break;
-                    default: val = I; break;
-                }
-                ep.pauli_out[t] = val;
             }
         }
+        if (!DB && i > 0) {
+            issue_load(w, tileb);
+            cp_async_commit();
+        }
+        cp_async_wait<0>();   // this item's tile has landed
+        __syncthreads();
+        QV_MARK(1);
+        if (DB && w + G < items) {   // stream the next item's tile in behind this one's math
+            issue_load(w + G, smem_raw + ((i & 1) ? 0 : TILE));
+            cp_async_commit();
+        }
+        // ---- register groups --------------------------------------------------
+        if (!zero_tile) {
+            for (int g = 0; g < pd.ng; ++g) {
+                if (active) {
+                    const GroupDesc& G = sg[g];
+                    uint32_t base = 0;
+#pragma unroll
+                    for (int m = 0; m < TB; ++m)
+                        if ((tid >> m) & 1) base ^= G.tcol[m];
+                    uint32_t off[NA];
+#pragma unroll
+                    for (int q = 0; q < NA / 4; ++q) {
+                        const uint4 c = reinterpret_cast<const uint4*>(G.combo)[q];
+                        off[4 * q] = base ^ c.x;
+                        off[4 * q + 1] = base ^ c.y;
+                        off[4 * q + 2] = base ^ c.z;
+                        off[4 * q + 3] = base ^ c.w;
+                    }
+                    const int4 mats = *reinterpret_cast<const int4*>(G.mat);
+                    V a[NA];
+#pragma unroll
+                    for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(tileb + off[j]);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
+                        if (mi >= 0) {
+                            const V* M = smat + mi * 4;
+                            const V m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
+#pragma unroll
+                            for (int j = 0; j < NA; ++j)
+                                if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
+                        }
+                    }
+                    if (g < 29) QV_MARK(2 + 2 * g);
+#pragma unroll
+                    for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(tileb + off[j]) = a[j];
+                }
+                // warp-local segment: the next group reads only what this warp wrote
+                if (g + 1 < pd.ng && !sg[g + 1].cta_sync) __syncwarp();
+                else __syncthreads();
+                if (g < 29) QV_MARK(3 + 2 * g);
+            }
+        }
+        // ---- store / reduce ----------------------------------------------------
+        double acc = 0.0;
+        if (active) {
+            V* __restrict__ dst = out + (outer | tg);
+#pragma unroll
+            for (int it = 0; it < NA; ++it) {
+                const V v = *reinterpret_cast<const V*>(tileb + (size_t)(fslot ^ pd.fin_hi[it]) * sizeof(V));
+                if (store) __stcs(dst + pd.g_hi[it], v);
+                acc += norm2(v);
+            }
+        }
+        QV_MARK(62);
+        if (ep.flags & F_NORM) {
+            const double s = block_sum(acc, sred);
+            if (tid == 0) ep.partial[e.pslot * ntiles + x] = s;
+        }
+        if (ep.flags & F_SUPPORT) {
+            const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
+            double* row = ep.sup_out + e.rslot * (ep.S + 1);
+            for (int32_t i = lo + tid; i < hi; i += blockDim.x) {
+                const uint32_t slot = apply_cols(pd.fin, K, (uint32_t)ep.sup_local[i]);
+                row[ep.sup_pos[i]] = norm2(*reinterpret_cast<const V*>(tileb + (size_t)slot * sizeof(V)));
+            }
+        }
+        if (ep.flags & F_SINGLE) {
+            // the tile is the whole state (ntiles == 1)
+            const double total = block_sum(acc, sred);
+            const int64_t dim = 1ll << ep.n;
+            if ((ep.flags & F_S_FULL) && active) {
+                double* row = ep.full_out + (e.rslot << ep.n);
+#pragma unroll
+                for (int it = 0; it < NA; ++it) {
+                    const uint32_t i = (uint32_t)tid | ((uint32_t)it << TB);
+                    if (i < dim)
+                        row[i] = norm2(*reinterpret_cast<const V*>(tileb + (size_t)(fslot ^ pd.fin_hi[it]) * sizeof(V))) / total;
+                }
+            }
+            if (ep.flags & (F_S_SUPPORT | F_S_JS)) {
+                double* row = (ep.flags & F_S_SUPPORT) ? ep.sup_out + e.rslot * (ep.S + 1) : nullptr;
+                double jsum = 0.0, qsum = 0.0;
+                for (int64_t s = tid; s < ep.S; s += blockDim.x) {
+                    const uint64_t idx = ep.support[s];
+                    double q = 0.0;
+                    if (idx < (uint64_t)dim)
+                        q = norm2(*reinterpret_cast<const V*>(tileb + (size_t)apply_cols(pd.fin, K, (uint32_t)idx) * sizeof(V))) / total;
+                    if (row) row[s] = q;
+                    if (ep.flags & F_S_JS) { jsum += js_term(ep.target[s], q); qsum += q; }
+                }
+                if (row && tid == 0) row[ep.S] = total;
+                if (ep.flags & F_S_JS) {
+                    const double J = block_sum(jsum, sred);
+                    const double Q = block_sum(qsum, sred);
+                    if (tid == 0) ep.js_out[e.rslot] = J + 0.5 * 0.69314718055994530942 * (1.0 - Q);
+                }
+            }
+            if (ep.flags & F_S_PAULI) {
+                const int64_t t0 = ep.term_off[e.rslot], t1 = ep.term_off[e.rslot + 1];
+                for (int64_t t = t0; t < t1; ++t) {
+                    const uint64_t F = ep.t_flip[t], PH = ep.t_phase[t];
+                    const uint32_t fF = apply_cols(pd.fin, K, (uint32_t)F);
+                    double ar = 0.0, ai = 0.0;
+                    if (active) {
+#pragma unroll
+                        for (int it = 0; it < NA; ++it) {
+                            const uint32_t i = (uint32_t)tid | ((uint32_t)it << TB);
+                            const uint32_t sl = fslot ^ pd.fin_hi[it];
+                            const V a = *reinterpret_cast<const V*>(tileb + (size_t)sl * sizeof(V));
+                            const V b = *reinterpret_cast<const V*>(tileb + (size_t)(sl ^ fF) * sizeof(V));
+                            // conj(b) * a
+                            const double tr = (double)b.x * (double)a.x + (double)b.y * (double)a.y;
+                            const double ti = (double)b.x * (double)a.y - (double)b.y * (double)a.x;
+                            if (__popcll((uint64_t)i & PH) & 1) { ar -= tr; ai -= ti; }
+                            else { ar += tr; ai += ti; }
+                        }
+                    }
+                    const double R = block_sum(ar, sred);
+                    const double I = block_sum(ai, sred);
+                    if (tid == 0) {
+                        const int ny = __popcll(F & PH) & 3;   // Y factors both flip and carry phase
+                        ep.pauli_out[t] = ny == 0 ? R : ny == 1 ? -I : ny == 2 ? -R : I;
+                    }
+                }
+            }
+        }
+        __syncthreads();   // the next tile overwrites the shared tile
     }
 }
 
@@ -327,8 +406,7 @@ __global__ void __launch_bounds__(256) pauli_sweep_kernel(const typename Cx<T>::
     const int64_t j0 = (int64_t)blockIdx.x * per_block;
     if (F == 0) {
         for (int64_t j = j0 + threadIdx.x; j < j0 + per_block; j += blockDim.x) {
-            const V a = st[j];
-            const double p = (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+            const double p = norm2(st[j]);
             if (__popcll((uint64_t)j & PH) & 1) ar -= p; else ar += p;
         }
     } else {
@@ -340,7 +418,7 @@ __global__ void __launch_bounds__(256) pauli_sweep_kernel(const typename Cx<T>::
             const V a = st[i], b = st[i2];
             const double tr = (double)b.x * (double)a.x + (double)b.y * (double)a.y;
             const double ti = (double)b.x * (double)a.y - (double)b.y * (double)a.x;
-            // term(i) = conj(b) a s(i); term(i2) = conj(a) b s(i2) = conj(term(i)) * s(i) s(i2)
+            // term(i) = conj(b) a s(i); term(i2) = conj(a) b s(i2) = conj(term(i)) s(i) s(i2)
             const double si = (__popcll(i & PH) & 1) ? -1.0 : 1.0;
             const double s2 = (__popcll(i2 & PH) & 1) ? -1.0 : 1.0;
             ar += si * tr + s2 * tr;
@@ -359,29 +437,18 @@ __global__ void finalize_pauli_kernel(const double2* __restrict__ partial, int64
     const double R = block_sum(ar, sred);
     const double I = block_sum(ai, sred);
     if (threadIdx.x == 0) {
-        double val;
-        switch (ny & 3) {
-            case 0: val = R; break;
-            case 1: val = -I; break;
-            case 2: val = -R; break;
-            default: val = I; break;
-        }
-        *out = val;
+        const int q = ny & 3;
+        *out = q == 0 ? R : q == 1 ? -I : q == 2 ? -R : I;
     }
 }
 
-}  // namespace qvb
-
-namespace qvb {
 // Multi-tile full distribution: p_i / total for a stored state.
 template <typename T>
 __global__ void full_probs_kernel(const typename Cx<T>::V* __restrict__ st, int64_t dim, const double* __restrict__ total,
                                   double* __restrict__ out) {
-    typedef typename Cx<T>::V V;
     const double t = *total;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x) {
-        const V a = st[i];
-        out[i] = ((double)a.x * (double)a.x + (double)a.y * (double)a.y) / t;
-    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = norm2(st[i]) / t;
 }
+
 }  // namespace qvb

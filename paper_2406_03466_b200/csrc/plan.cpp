@@ -125,10 +125,22 @@ std::vector<PassPlan> select_passes(int n, int k, int c, const std::vector<Fused
     return passes;
 }
 
+// Builds the register groups of one pass.  Groups are first recorded with the
+// slot map Q in force when they are applied; `emit` then splits them into
+// warp-local segments and writes the device descriptors.
 struct GroupBuilder {
     int k, beta;
+    int rbits;             // register bits per group (reg_bits(precision))
+    int amp_shift;         // log2(bytes per amplitude): 4 complex128, 3 complex64
     uint16_t col[16];      // logical-bit -> slot column (before swizzle): the map Q
     std::vector<std::pair<int, int>> open;  // (logical bit, pass-local matrix index)
+
+    struct Pending {
+        std::vector<std::pair<int, int>> ops;  // (bit, matrix)
+        uint16_t col[16];                      // Q when the group is applied
+        uint32_t targets_after = 0;            // CNOT targets applied before the next group
+    };
+    std::vector<Pending> pending;
 
     uint16_t swz(uint32_t v) const {   // bank swizzle, GF(2)-linear
         uint32_t r = v;
@@ -138,47 +150,99 @@ struct GroupBuilder {
     }
     uint16_t phys(int b) const { return swz(col[b]); }
 
-    void close(std::vector<GroupDesc>& out) {
+    void close() {
         if (open.empty()) return;
-        GroupDesc g;
-        std::memset(&g, 0, sizeof(g));
-        int reg[kRegBits];
-        uint32_t used = 0;
-        int nr = 0;
-        for (auto& pr : open) { reg[nr] = pr.first; g.mat[nr] = (int16_t)pr.second; used |= 1u << pr.first; ++nr; }
-        for (int b = k - 1; b >= 0 && nr < kRegBits; --b)
-            if (!((used >> b) & 1u)) { reg[nr] = b; g.mat[nr] = -1; used |= 1u << b; ++nr; }
-        // complement bits -> thread bits; the first `beta` of them index the
-        // lanes of one shared-memory wavefront, pick them with independent
-        // bank projections so those accesses are conflict-free
-        std::vector<int> comp;
-        for (int b = 0; b < k; ++b)
-            if (!((used >> b) & 1u)) comp.push_back(b);
+        Pending p;
+        p.ops = open;
+        std::memcpy(p.col, col, sizeof(col));
+        pending.push_back(p);
+        open.clear();
+    }
+
+    void cnot(int c, int t) {
+        col[c] ^= col[t];   // Q <- Q o CNOT
+        if (!pending.empty()) pending.back().targets_after |= 1u << t;
+    }
+
+    // Order `cand` so its first `beta` entries have linearly independent
+    // shared-memory bank projections under column map `cols` (one wavefront
+    // of lanes is then conflict-free).
+    std::vector<int> bank_order(const std::vector<int>& cand, const uint16_t* cols) const {
         std::vector<int> order;
-        std::vector<bool> taken(comp.size(), false);
+        std::vector<bool> taken(cand.size(), false);
         const uint32_t bmask = (1u << beta) - 1;
         uint32_t span = 1u;   // set of bank indices spanned so far ({0})
-        for (size_t i = 0; i < comp.size() && (int)order.size() < beta; ++i) {
-            const uint32_t v = phys(comp[i]) & bmask;
-            if ((span >> v) & 1u) continue;   // dependent on the lanes chosen so far
+        for (size_t i = 0; i < cand.size() && (int)order.size() < beta; ++i) {
+            const uint32_t v = swz(cols[cand[i]]) & bmask;
+            if ((span >> v) & 1u) continue;
             uint32_t grown = span;
             for (uint32_t e = 0; e <= bmask; ++e)
                 if ((span >> e) & 1u) grown |= 1u << (e ^ v);
             span = grown;
-            order.push_back(comp[i]);
+            order.push_back(cand[i]);
             taken[i] = true;
         }
-        for (size_t i = 0; i < comp.size(); ++i)
-            if (!taken[i]) order.push_back(comp[i]);
-        for (int j = 0; j < kGroupAmps; ++j) {
-            uint16_t s = 0;
-            for (int r = 0; r < kRegBits; ++r)
-                if ((j >> r) & 1) s ^= phys(reg[r]);
-            g.combo[j] = s;
+        for (size_t i = 0; i < cand.size(); ++i)
+            if (!taken[i]) order.push_back(cand[i]);
+        return order;
+    }
+
+    void emit(std::vector<GroupDesc>& out) {
+        const int tb = k - rbits;
+        const int nwb = tb > 5 ? tb - 5 : 0;           // warp-index bits
+        const uint32_t all = (1u << k) - 1;
+        // segments: maximal runs of groups that leave >= nwb bits untouched
+        // (no matrix, no CNOT target in between); those bits index the warp
+        std::vector<uint32_t> wmask(pending.size(), 0);
+        std::vector<int> seg_start(pending.size(), 0);
+        size_t s = 0;
+        while (s < pending.size()) {
+            uint32_t free_bits = all;
+            for (auto& pr : pending[s].ops) free_bits &= ~(1u << pr.first);
+            size_t e = s + 1;
+            while (e < pending.size()) {
+                uint32_t f = free_bits & ~pending[e - 1].targets_after;
+                for (auto& pr : pending[e].ops) f &= ~(1u << pr.first);
+                if (__builtin_popcount(f) < nwb) break;
+                free_bits = f;
+                ++e;
+            }
+            uint32_t w = 0;   // the highest free bits become the warp index
+            for (int b = k - 1; b >= 0 && __builtin_popcount(w) < nwb; --b)
+                if ((free_bits >> b) & 1u) w |= 1u << b;
+            for (size_t g = s; g < e; ++g) { wmask[g] = w; seg_start[g] = g == s; }
+            s = e;
         }
-        for (size_t m = 0; m < order.size(); ++m) g.tcol[m] = phys(order[m]);
-        out.push_back(g);
-        open.clear();
+        for (size_t gi = 0; gi < pending.size(); ++gi) {
+            const Pending& p = pending[gi];
+            GroupDesc g;
+            std::memset(&g, 0, sizeof(g));
+            int reg[kRegBits];
+            uint32_t used = 0;
+            int nr = 0;
+            for (int r = 0; r < kRegBits; ++r) g.mat[r] = -1;
+            for (auto& pr : p.ops) { reg[nr] = pr.first; g.mat[nr] = pr.second; used |= 1u << pr.first; ++nr; }
+            for (int b = k - 1; b >= 0 && nr < rbits; --b)   // pad with bits outside the warp index
+                if (!((used >> b) & 1u) && !((wmask[gi] >> b) & 1u)) { reg[nr] = b; g.mat[nr] = -1; used |= 1u << b; ++nr; }
+            std::vector<int> lanes, warps;
+            for (int b = 0; b < k; ++b) {
+                if ((used >> b) & 1u) continue;
+                if ((wmask[gi] >> b) & 1u) warps.push_back(b);
+                else lanes.push_back(b);
+            }
+            std::vector<int> order = bank_order(lanes, p.col);
+            order.insert(order.end(), warps.begin(), warps.end());
+            for (int j = 0; j < (1 << rbits); ++j) {
+                uint32_t sl = 0;
+                for (int r = 0; r < rbits; ++r)
+                    if ((j >> r) & 1) sl ^= swz(p.col[reg[r]]);
+                g.combo[j] = sl << amp_shift;
+            }
+            for (size_t m = 0; m < order.size(); ++m) g.tcol[m] = (uint32_t)swz(p.col[order[m]]) << amp_shift;
+            g.cta_sync = (gi == 0 || seg_start[gi]) ? 1 : 0;
+            out.push_back(g);
+        }
+        pending.clear();
     }
 };
 
@@ -198,8 +262,8 @@ std::string Topology::key() const {
 }
 
 int tile_bits_for(int n, int precision) {
-    const int kmax = precision == 0 ? 12 : 13;
-    if (n <= kmax) return std::max(n, kRegBits);
+    const int kmax = max_tile_bits(precision);
+    if (n <= kmax) return std::max(n, reg_bits(precision));
     return kmax;
 }
 
@@ -211,7 +275,7 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
     if (max_tile_bits > 0) {
         if (max_tile_bits < coalesce_bits(precision) + 2 || max_tile_bits > kMaxTileBits)
             throw std::runtime_error("tile bits out of range");
-        plan.k = topo.n <= max_tile_bits ? std::max(topo.n, kRegBits) : max_tile_bits;
+        plan.k = topo.n <= max_tile_bits ? std::max(topo.n, reg_bits(precision)) : max_tile_bits;
     }
     plan.single_tile = topo.n <= plan.k;
     plan.ops = fuse(topo);
@@ -238,42 +302,93 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
             for (int b = 0; b < n; ++b)
                 if (logical_of[b] < 0) d.obits[o++] = (uint8_t)b;
         }
+        const int R = reg_bits(precision);
         GroupBuilder gb;
         gb.k = k;
         gb.beta = beta;
+        gb.rbits = R;
+        gb.amp_shift = precision == 0 ? 4 : 3;
         for (int j = 0; j < 16; ++j) gb.col[j] = (uint16_t)(j < k ? 1u << j : 0);
         for (int j = 0; j < k; ++j) d.swz[j] = gb.phys(j);
         d.g0 = (int)plan.groups.size();
         d.m0 = (int)plan.mat_op.size();
         int local_mats = 0;
-        for (int oi : pp.ops) {
-            const FusedOp& op = plan.ops[oi];
-            if (!op.cnot) {
-                const int lb = logical_of[op.b0];
-                bool clash = false;
-                for (auto& pr : gb.open) clash |= pr.first == lb;
-                if (clash || (int)gb.open.size() == kRegBits) gb.close(plan.groups);
-                gb.open.push_back({lb, local_mats++});
-                plan.mat_op.push_back(oi);
-            } else {
-                const int lc = logical_of[op.b0], lt = logical_of[op.b1];
-                bool clash = false;
-                for (auto& pr : gb.open) clash |= pr.first == lc || pr.first == lt;
-                if (clash) gb.close(plan.groups);
-                gb.col[lc] ^= gb.col[lt];   // Q <- Q o CNOT
+        // List scheduling of the pass's op DAG (edges: program order on shared
+        // bits).  Ready CNOTs are folded into Q immediately (free); register
+        // groups are filled with up to R ready MAT1s, longest remaining
+        // dependency chain first, so groups are full and few.
+        const int m = (int)pp.ops.size();
+        std::vector<std::vector<int>> preds(m), succs(m);
+        {
+            std::vector<int> last(64, -1);
+            for (int i = 0; i < m; ++i) {
+                const FusedOp& op = plan.ops[pp.ops[i]];
+                const int bits[2] = {op.b0, op.cnot ? op.b1 : -1};
+                for (int b : bits) {
+                    if (b < 0) continue;
+                    if (last[b] >= 0) { preds[i].push_back(last[b]); succs[last[b]].push_back(i); }
+                    last[b] = i;
+                }
             }
         }
-        gb.close(plan.groups);
+        std::vector<int> height(m, 0);
+        for (int i = m - 1; i >= 0; --i)
+            for (int s : succs[i]) height[i] = std::max(height[i], height[s] + 1);
+        std::vector<char> applied(m, 0), in_group(m, 0);
+        std::vector<int> open_ops;
+        int done = 0;
+        auto ready = [&](int i) {
+            for (int p : preds[i])
+                if (!applied[p]) return false;
+            return true;
+        };
+        auto close_group = [&]() {
+            gb.close();
+            for (int i : open_ops) { applied[i] = 1; ++done; }
+            open_ops.clear();
+        };
+        while (done < m) {
+            bool progress = true;
+            while (progress) {   // fold every ready CNOT into the slot map
+                progress = false;
+                for (int i = 0; i < m; ++i) {
+                    const FusedOp& op = plan.ops[pp.ops[i]];
+                    if (!op.cnot || applied[i] || !ready(i)) continue;
+                    gb.cnot(logical_of[op.b0], logical_of[op.b1]);
+                    applied[i] = 1;
+                    ++done;
+                    progress = true;
+                }
+            }
+            if (done == m) break;
+            int best = -1;
+            for (int i = 0; i < m; ++i) {
+                if (plan.ops[pp.ops[i]].cnot || applied[i] || in_group[i] || !ready(i)) continue;
+                if (best < 0 || height[i] > height[best]) best = i;
+            }
+            if (best < 0) {
+                if (open_ops.empty()) throw std::runtime_error("group scheduler stalled");
+                close_group();
+                continue;
+            }
+            in_group[best] = 1;
+            open_ops.push_back(best);
+            gb.open.push_back({logical_of[plan.ops[pp.ops[best]].b0], local_mats++});
+            plan.mat_op.push_back(pp.ops[best]);
+            if ((int)open_ops.size() == R) close_group();
+        }
+        close_group();
+        gb.emit(plan.groups);
         d.ng = (int)plan.groups.size() - d.g0;
         d.nm = local_mats;
         for (int j = 0; j < k; ++j) d.fin[j] = gb.phys(j);
-        for (int it = 0; it < 16; ++it) {
-            const uint32_t idx = (uint32_t)it << (k - kRegBits);
+        for (int it = 0; it < (1 << R); ++it) {   // a thread's amplitudes: tid | it << (k - R)
+            const uint32_t idx = (uint32_t)it << (k - R);
             d.swz_hi[it] = (uint16_t)apply_cols(d.swz, k, idx);
             d.fin_hi[it] = (uint16_t)apply_cols(d.fin, k, idx);
             uint64_t g = 0;
-            for (int i = 0; i < kRegBits; ++i)
-                if ((it >> i) & 1) g |= 1ull << d.sbits[k - kRegBits + i];
+            for (int i = 0; i < R; ++i)
+                if ((it >> i) & 1) g |= 1ull << d.sbits[k - R + i];
             d.g_hi[it] = g;
         }
         pp.n_groups = d.ng;

@@ -17,8 +17,26 @@
 
 namespace qvb {
 
-constexpr int kRegBits = 4;          // register bits per group: 16 amplitudes per thread
+constexpr int kRegBits = 4;          // max register bits per group (descriptor capacity)
 constexpr int kGroupAmps = 1 << kRegBits;
+
+// Register bits per group (amplitudes per thread = 2^R).  complex128 uses 3
+// (8 amplitudes, ~100 registers) so a 4096-amplitude tile runs on 512 threads
+// = 16 warps per SM: FP64 latency (8 cycles, one DFMA per ~2.3 cycles per
+// warp, measured) needs >= 2 warps per scheduler in their math phase.
+// complex64 uses 4 (16 amplitudes) over 8192-amplitude tiles.
+#ifndef QV_C128_REG_BITS
+#define QV_C128_REG_BITS 4
+#endif
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr int reg_bits(int precision) { return precision == 0 ? QV_C128_REG_BITS : 4; }
+// widest tile (multi-tile registers): 2^12 complex128 / 2^13 complex64 = 64 KiB
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr int max_tile_bits(int precision) { return precision == 0 ? 12 : 13; }
 constexpr int kMaxTileBits = 13;     // 2^13 amplitudes (64 KiB at complex64, 128 KiB c128)
 constexpr int kMaxQubits = 40;
 
@@ -46,14 +64,22 @@ struct FusedOp {
 
 // Device descriptor of one register group: a thread loads 16 amplitudes from
 // physical shared-memory slots base(tid) ^ combo[j], applies up to 4 2x2
-// matrices on register bits 0..3 and stores them back.
+// matrices on register bits 0..3 and stores them back.  Slots are stored as
+// BYTE offsets for the state's amplitude size so the kernel XORs them
+// straight into a shared-memory address.
+//
+// Thread bits 0..4 are the lanes of a warp, bits 5.. the warp index.  The
+// planner keeps the warp-index bits of consecutive groups equal and untouched
+// by their matrices and CNOT targets wherever it can ("warp-local segments"):
+// every warp then reads back exactly the amplitudes it wrote, and the groups
+// are separated by __syncwarp instead of a CTA barrier (`cta_sync` = 0).
 struct alignas(16) GroupDesc {
-    uint16_t combo[16];
-    uint16_t tcol[10];   // physical column of thread bit m (tile bits - 4 of them)
-    int16_t mat[4];      // matrix index within the pass (-1 = identity)
-    uint16_t pad[2];
+    uint32_t combo[16];  // byte offset of register index j
+    uint32_t tcol[11];   // byte offset of thread bit m (tile bits - 4 of them)
+    int32_t cta_sync;    // 1: a CTA barrier must precede this group
+    int32_t mat[4];      // matrix index within the pass (-1 = identity)
 };
-static_assert(sizeof(GroupDesc) == 64, "GroupDesc layout");
+static_assert(sizeof(GroupDesc) == 128, "GroupDesc layout");
 
 // Device descriptor of one pass (one HBM sweep over every tile of a state).
 struct alignas(16) PassDesc {

@@ -5,6 +5,7 @@
 // the host with std::complex<double>, so CPU tests can check the planner's
 // GF(2) bookkeeping against the oracle without a GPU.  The product library
 // (libqvb200.so) does not contain this code and never calls it.
+#include <algorithm>
 #include <complex>
 #include <cstring>
 #include <exception>
@@ -39,7 +40,8 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
         const Plan plan = build_plan(topo, precision, max_tile_bits);
         std::vector<double> mats((size_t)plan.n_slots() * 8);
         circuit_matrices(plan, topo, angles, mats.data());
-        const int k = plan.k, tb = k - kRegBits, nt = 1 << tb;
+        const int R = reg_bits(precision), NA = 1 << R;
+        const int k = plan.k, tb = k - R, nt = 1 << tb;
         const size_t dim = (size_t)1 << std::max(n, k);
         std::vector<cd> st(dim, cd(0, 0)), tile((size_t)1 << k);
         st[0] = 1.0;
@@ -54,28 +56,43 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
                     uint64_t tg = 0;
                     for (int j = 0; j < tb; ++j)
                         if ((tid >> j) & 1) { ts ^= pd.swz[j]; tg |= 1ull << pd.sbits[j]; }
-                    for (int it = 0; it < 16; ++it) tile[ts ^ pd.swz_hi[it]] = st[outer | tg | pd.g_hi[it]];
+                    for (int it = 0; it < NA; ++it) tile[ts ^ pd.swz_hi[it]] = st[outer | tg | pd.g_hi[it]];
                 }
+                const int sh = precision == 0 ? 4 : 3;   // descriptors hold byte offsets
+                // warp-local segments: without a CTA barrier, every warp must touch
+                // exactly the slots it touched in the previous group
+                std::vector<std::vector<uint32_t>> prev_sets;
                 for (int g = pd.g0; g < pd.g0 + pd.ng; ++g) {
                     const GroupDesc& G = plan.groups[g];
+                    const int nwarps = (nt + 31) / 32;
+                    std::vector<std::vector<uint32_t>> sets(nwarps);
+                    for (int tid = 0; tid < nt; ++tid) {
+                        uint32_t base = 0;
+                        for (int m = 0; m < tb; ++m)
+                            if ((tid >> m) & 1) base ^= G.tcol[m];
+                        for (int j = 0; j < NA; ++j) sets[tid / 32].push_back(base ^ G.combo[j]);
+                    }
+                    for (auto& s : sets) std::sort(s.begin(), s.end());
+                    if (g > pd.g0 && !G.cta_sync && sets != prev_sets) return -2;
+                    prev_sets = sets;
                     for (int tid = 0; tid < nt; ++tid) {
                         uint32_t base = 0;
                         for (int m = 0; m < tb; ++m)
                             if ((tid >> m) & 1) base ^= G.tcol[m];
                         cd a[16];
-                        for (int j = 0; j < 16; ++j) a[j] = tile[base ^ G.combo[j]];
-                        for (int r = 0; r < kRegBits; ++r) {
+                        for (int j = 0; j < NA; ++j) a[j] = tile[(base ^ G.combo[j]) >> sh];
+                        for (int r = 0; r < R; ++r) {
                             if (G.mat[r] < 0) continue;
                             const double* M = mats.data() + (size_t)(pd.m0 + G.mat[r]) * 8;
                             const cd m00(M[0], M[1]), m01(M[2], M[3]), m10(M[4], M[5]), m11(M[6], M[7]);
-                            for (int j = 0; j < 16; ++j) {
+                            for (int j = 0; j < NA; ++j) {
                                 if ((j >> r) & 1) continue;
                                 const cd u = a[j], v = a[j | (1 << r)];
                                 a[j] = m00 * u + m01 * v;
                                 a[j | (1 << r)] = m10 * u + m11 * v;
                             }
                         }
-                        for (int j = 0; j < 16; ++j) tile[base ^ G.combo[j]] = a[j];
+                        for (int j = 0; j < NA; ++j) tile[(base ^ G.combo[j]) >> sh] = a[j];
                     }
                 }
                 for (int tid = 0; tid < nt; ++tid) {
@@ -83,7 +100,7 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
                     uint64_t tg = 0;
                     for (int j = 0; j < tb; ++j)
                         if ((tid >> j) & 1) { fs ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
-                    for (int it = 0; it < 16; ++it) st[outer | tg | pd.g_hi[it]] = tile[fs ^ pd.fin_hi[it]];
+                    for (int it = 0; it < NA; ++it) st[outer | tg | pd.g_hi[it]] = tile[fs ^ pd.fin_hi[it]];
                 }
             }
         }
@@ -95,7 +112,8 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
 }
 
 // Plan shape: stats[0] passes, [1] groups, [2] matrix slots, [3] fused ops,
-// [4] tile bits, [5] single tile; per-pass matrices in pass_mats (if non-null, <= cap).
+// [4] tile bits, [5] single tile, [6] groups needing a CTA barrier;
+// per-pass matrices in pass_mats (if non-null, <= cap).
 int qvp_plan_stats(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1, int precision,
                    int max_tile_bits, int64_t* stats, int32_t* pass_mats, int32_t cap) {
     try {
@@ -107,6 +125,9 @@ int qvp_plan_stats(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* 
         stats[3] = (int64_t)plan.ops.size();
         stats[4] = plan.k;
         stats[5] = plan.single_tile ? 1 : 0;
+        int64_t syncs = 0;
+        for (const GroupDesc& g : plan.groups) syncs += g.cta_sync;
+        stats[6] = syncs;
         if (pass_mats)
             for (size_t p = 0; p < plan.pdesc.size() && (int32_t)p < cap; ++p) pass_mats[p] = plan.pdesc[p].nm;
         return 0;

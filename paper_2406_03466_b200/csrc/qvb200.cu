@@ -17,7 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
+#include <utility>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -253,18 +255,87 @@ struct GroupRun {
 };
 
 template <typename T>
+using PassFn = void (*)(const PassDesc, const GroupDesc*, const LaunchEntry*, int, int, EpiArgs);
+
+template <typename T, int... TBs>
+constexpr std::array<PassFn<T>, sizeof...(TBs)> pass_table(std::integer_sequence<int, TBs...>) {
+    return {{&pass_kernel<T, TBs, false>...}};
+}
+// TB = tile bits - 4: 0..8 for complex128 (k <= 12), 0..9 for complex64 (k <= 13)
+template <typename T>
+const std::array<PassFn<T>, 10>& pass_kernels() {
+    static const std::array<PassFn<T>, 10> table = pass_table<T>(std::make_integer_sequence<int, 10>{});
+    return table;
+}
+// double-buffered variant used for multi-tile states (widest tile)
+template <typename T>
+constexpr int multi_tile_tb() {
+    return max_tile_bits(sizeof(T) == 8 ? 0 : 1) - reg_bits(sizeof(T) == 8 ? 0 : 1);
+}
+template <typename T>
+PassFn<T> pass_kernel_db() {
+    return &pass_kernel<T, multi_tile_tb<T>(), true>;
+}
+
+template <typename T>
+void set_kernel_attributes() {
+    for (auto fn : pass_kernels<T>())
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(pass_kernel_db<T>(), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+}
+
+template <typename T>
 void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const LaunchEntry* d_ent, int nstates,
                  int64_t ntiles, const EpiArgs& ep, bool generated) {
     typedef typename Cx<T>::V V;
-    constexpr int NT = sizeof(T) == 8 ? kNT128 : kNT64;
-    const size_t smem = (sizeof(V) << pd.k) + (size_t)pd.ng * sizeof(GroupDesc) + (size_t)pd.nm * 8 * sizeof(T) + 32 * sizeof(double);
-    const int threads = std::max(32, 1 << (pd.k - kRegBits));
-    const int64_t blocks = ntiles * nstates;
-    if (blocks > 0x7fffffffll) throw ArgError("launch too large");
+    const int tb = pd.k - reg_bits(sizeof(T) == 8 ? 0 : 1);
+    const bool db = ntiles > 1 && tb == multi_tile_tb<T>();
+    const size_t smem = (sizeof(V) << pd.k) * (db ? 2 : 1) + (size_t)pd.ng * sizeof(GroupDesc) +
+                        (size_t)pd.nm * 4 * sizeof(V) + 32 * sizeof(double);
+    const int threads = pass_threads(tb);
+    PassFn<T> fn = db ? pass_kernel_db<T>() : pass_kernels<T>()[tb];
+    // persistent CTAs: enough per state to fill every SM at full occupancy
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+    per_sm = std::max(per_sm, 1);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E.device));
+    const int64_t slots = (int64_t)per_sm * sms;
+    const int64_t blocks = std::min<int64_t>(ntiles * nstates, slots);   // exactly one persistent wave
+    EpiArgs e2 = ep;
+    e2.ntiles = ntiles;
+    e2.trace = nullptr;
+#ifdef QV_TRACE
+    // debug builds: record a per-phase clock64() timeline of CTA 0 for the
+    // first launch with >= 8 items per CTA; written to $QVB200_TRACE_OUT
+    static bool traced = false;
+    long long* d_trace = nullptr;
+    const bool do_trace = !traced && pd.m0 > 0 && ntiles * nstates >= 8 * blocks && getenv("QVB200_TRACE_OUT");
+    if (do_trace) {
+        CK(cudaMalloc(&d_trace, 8 * 64 * 16 * sizeof(long long)));
+        CK(cudaMemsetAsync(d_trace, 0, 8 * 64 * 16 * sizeof(long long), E.stream));
+        e2.trace = d_trace;
+    }
+#endif
     cudaEvent_t e0 = E.next_event(), e1 = E.next_event();
     CK(cudaEventRecord(e0, E.stream));
-    pass_kernel<T, NT><<<(unsigned)blocks, threads, smem, E.stream>>>(pd, d_groups, d_ent, nstates, ep);
+    fn<<<(unsigned)blocks, threads, smem, E.stream>>>(pd, d_groups, d_ent, nstates, 0, e2);
     CK(cudaGetLastError());
+#ifdef QV_TRACE
+    if (do_trace) {
+        std::vector<long long> h(8 * 64 * 16);
+        CK(cudaStreamSynchronize(E.stream));
+        CK(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        cudaFree(d_trace);
+        traced = true;
+        if (FILE* f = fopen(getenv("QVB200_TRACE_OUT"), "wb")) {
+            const int hdr[4] = {pd.k, pd.ng, pd.nm, threads};
+            fwrite(hdr, sizeof(int), 4, f);
+            fwrite(h.data(), sizeof(long long), h.size(), f);
+            fclose(f);
+        }
+    }
+#endif
     CK(cudaEventRecord(e1, E.stream));
     E.timed.push_back({e0, e1});
     E.stats[0] += 1;
@@ -734,8 +805,8 @@ int qv_create(int device, int precision, uint64_t memory_budget_bytes, qv_handle
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
         E->budget = memory_budget_bytes ? memory_budget_bytes : (uint64_t)(0.85 * (double)free_b);
-        CK(cudaFuncSetAttribute(pass_kernel<double, kNT128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CK(cudaFuncSetAttribute(pass_kernel<float, kNT64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        set_kernel_attributes<double>();
+        set_kernel_attributes<float>();
         *out = reinterpret_cast<qv_handle>(E);
         return QV_OK;
     } catch (const std::exception&) {

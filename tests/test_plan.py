@@ -47,7 +47,7 @@ def simulate(lib, n, gates, tile_bits, precision=0):
 
 def stats(lib, n, gates, tile_bits=0, precision=0):
     kinds, q0, q1, _ = arrays(gates)
-    st = np.zeros(6, np.int64)
+    st = np.zeros(7, np.int64)
     pm = np.zeros(256, np.int32)
     assert lib.qvp_plan_stats(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data,
                               precision, tile_bits, st.ctypes.data, pm.ctypes.data, 256) == 0
@@ -76,6 +76,30 @@ def test_ddcl_layers_multi_pass(plan_lib, n, layers, tile):
     got, passes = simulate(plan_lib, n, gates, tile)
     assert passes > 1
     assert np.max(np.abs(got - sv.run_gates(n, gates))) < 1e-12
+
+
+@pytest.mark.parametrize("n,layers,precision", [(13, 2, 0), (14, 2, 1), (16, 1, 0), (15, 1, 1)])
+def test_ddcl_production_tiles_and_warp_local_segments(plan_lib, n, layers, precision):
+    """Production tile sizes (k = 12 / 13: 8 / 16 warps).  The interpreter
+    returns -2 if a group without a CTA barrier makes any warp touch slots
+    other than the ones it wrote in the previous group."""
+    gates = sv.bind_template(sv.ddcl_template_gates(n, layers), sv.random_angles(6 * n * layers, n))
+    got, passes = simulate(plan_lib, n, gates, 0, precision)
+    assert passes > 1
+    assert np.max(np.abs(got - sv.run_gates(n, gates))) < 1e-12
+    st, _ = stats(plan_lib, n, gates, 0, precision)
+    assert st[6] < st[1]   # some groups are warp-local
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_circuits_multi_warp_tiles(plan_lib, seed):
+    rng = np.random.Generator(np.random.PCG64(100 + seed))
+    n = 13 + seed % 2
+    gates = sv.random_circuit_gates(rng, n, 120, extended=True)
+    want = sv.run_gates(n, gates)
+    for tile, precision in ((10, 0), (11, 1), (0, 0), (0, 1)):
+        got, _ = simulate(plan_lib, n, gates, tile, precision)
+        assert np.max(np.abs(got - want)) < 1e-12, (tile, precision)
 
 
 def test_pass_counts_for_baseline_configs(plan_lib):
