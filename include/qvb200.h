@@ -120,6 +120,24 @@ int qv_destroy(qv_handle handle);
 int qv_execute(qv_handle handle, const qv_circuits* circuits, const qv_results* results,
                double* out, int64_t out_len);
 
+/* Parameter-shift JS losses of ONE bound circuit without simulating two
+ * shifted circuits per parameter.  For a rotation gate g (RX/RY/RZ, generator
+ * P) at angle t, R(t +- pi/2) = R(t) (I -+ iP) / sqrt(2) exactly, so the two
+ * shifted output states are (Psi0 -+ i Xi_g) / sqrt(2): Psi0 is the
+ * unshifted output and Xi_g the output with P inserted at gate g.  One extra
+ * state per shifted gate replaces two circuits; the two distributions are
+ * formed in the final pass's epilogue.  Replaces the loss loop of reference
+ * ddcl.py:210-225 over gradients.py:33-46 (theta[k] +- pi/2 for every k).
+ *   base        : n_circuits = 1
+ *   gate_index  : n_shift rotation-gate indices into base's gate list
+ *   results     : kind = QV_OUT_JS (support + target)
+ *   out         : 2 * n_shift doubles, out[2j] = JS at t_j + pi/2, out[2j+1] = JS at t_j - pi/2
+ * Results agree with direct simulation of the shifted circuits to FP64
+ * rounding (~1e-16), not bitwise; requires a register wider than one tile
+ * (n > 12 complex128, n > 13 complex64), returns QV_ERR_ARGUMENT otherwise. */
+int qv_shift_js(qv_handle handle, const qv_circuits* base, int64_t n_shift, const int64_t* gate_index,
+                const qv_results* results, double* out);
+
 /* Last error of this handle (empty string if none) and the index of the
  * circuit it belongs to (-1 if it is not specific to one circuit). */
 const char* qv_last_error(qv_handle handle);

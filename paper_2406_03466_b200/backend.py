@@ -32,7 +32,7 @@ from typing import Iterable, Mapping, Protocol, Sequence
 import numpy as np
 
 from . import native
-from .ir import CODE_BY_VALUE, Circuit
+from .ir import CODE_BY_VALUE, Circuit, bind
 from .observables import Observable, PauliTerm, term_masks
 from .results import ChildResult, ResultBuffer
 
@@ -245,6 +245,44 @@ class B200Backend:
         out = self._run(lowered, n_qubits, native.QV_OUT_JS, circuits, support=sup, target=p)
         self.gate_counter += _gate_count(circuits)
         return out
+
+    def shift_js_losses(self, template: Circuit, theta: Sequence[float], target: Mapping[str, float],
+                        params: Sequence[int]) -> np.ndarray:
+        """JS losses of the circuits with theta[k] + pi/2 and theta[k] - pi/2,
+        for each k in `params`: [2 * len(params)], '+' then '-' per parameter.
+
+        Uses R(t +- pi/2) = R(t)(I -+ iP)/sqrt2: the unshifted output Psi0 plus
+        ONE extra state per parameter (P inserted at the parameter's gate)
+        replace the two shifted circuits (qv_shift_js).  Exact up to FP64
+        rounding; each parameter must feed exactly one rotation gate, and the
+        register must span several tiles (otherwise use `js_losses`)."""
+        n = template.n_qubits
+        lw = template.lowering()
+        gate_of = np.full(lw.n_params, -1, np.int64)
+        for g, k in enumerate(lw.param_index.tolist()):
+            if k >= 0:
+                if gate_of[k] >= 0:
+                    raise ValueError(f"parameter {k} feeds several gates; shift pairs need one gate per parameter")
+                gate_of[k] = g
+        ks = np.asarray(params, dtype=np.int64)
+        if np.any(gate_of[ks] < 0):
+            raise ValueError("a shifted parameter feeds no gate")
+        base = lower_batch([bind(template, theta)])
+        keys = sorted(target)
+        sup = support_indices(keys, n)
+        p = np.asarray([float(target[k]) for k in keys], dtype=np.float64)
+        name = template.name
+        try:
+            out = self._engine.shift_js(n, base, gate_of[ks], sup, p)
+        except native.NativeError as err:
+            raise ExecutionError(name, str(err)) from err
+        self.last_stats = dict(self._engine.last_stats)
+        self.gate_counter += 2 * len(ks) * int(lw.kinds.shape[0])
+        return out
+
+    def tile_qubits(self) -> int:
+        """Widest register simulated inside one CTA's shared memory."""
+        return 12 if self.precision == "complex128" else 13
 
     # -- internals -----------------------------------------------------------
     def _precheck(self, c, n: int, children: bool = True) -> str:

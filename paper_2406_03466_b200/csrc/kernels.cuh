@@ -32,6 +32,7 @@ enum EpiFlags : int {
     F_S_JS = 32,       // single: JS loss
     F_S_FULL = 64,     // single: all normalised probabilities
     F_S_PAULI = 128,   // single: Pauli terms
+    F_PAIR = 256,      // multi-tile: shift-pair epilogue over (Psi0 = aux, Xi = this tile)
 };
 
 struct LaunchEntry {
@@ -40,7 +41,7 @@ struct LaunchEntry {
     const void* mats;   // matrix table of this state (slot 0)
     int64_t rslot;      // result slot (outputs)
     int64_t pslot;      // partial-sum slot (multi-tile norm partials)
-    int64_t pad;
+    const void* aux;    // F_PAIR: the unshifted output state Psi0
 };
 
 struct EpiArgs {
@@ -61,6 +62,7 @@ struct EpiArgs {
     const uint64_t* t_flip;
     const uint64_t* t_phase;
     double* pauli_out;         // [term]
+    double* pair_sup;          // F_PAIR: [(rslot * S + pos) * 3 + {|Psi0|^2, |Xi|^2, Im(Psi0 conj Xi)}]
     long long* trace;          // QV_TRACE builds only: per-phase clock64() of CTA 0
 };
 
@@ -284,7 +286,47 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         }
         // ---- store / reduce ----------------------------------------------------
         double acc = 0.0;
-        if (active) {
+        if (ep.flags & F_PAIR) {
+            // shift pair: this tile holds Xi, `aux` the unshifted output Psi0.
+            // Per tile: sum |Psi0|^2, sum |Xi|^2, sum Im(Psi0 conj(Xi)); per
+            // support index the same three terms (finalize_pair_kernel forms
+            // p(t +- pi/2) = |Psi0 -+ i Xi|^2 / 2 from them).
+            const V* __restrict__ aux = reinterpret_cast<const V*>(e.aux);
+            double accB = 0.0, accC = 0.0;
+            if (active) {
+                const V* __restrict__ src = aux + (outer | tg);
+#pragma unroll
+                for (int it = 0; it < NA; ++it) {
+                    const V v = *reinterpret_cast<const V*>(tileb + (size_t)(fslot ^ pd.fin_hi[it]) * sizeof(V));
+                    const V u = __ldcs(src + pd.g_hi[it]);
+                    acc += norm2(u);
+                    accB += norm2(v);
+                    accC += (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+                }
+            }
+            const double A = block_sum(acc, sred);
+            const double B = block_sum(accB, sred);
+            const double C = block_sum(accC, sred);
+            if (tid == 0) {
+                double* p = ep.partial + (e.pslot * ntiles + x) * 3;
+                p[0] = A;
+                p[1] = B;
+                p[2] = C;
+            }
+            const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
+            for (int32_t q = lo + tid; q < hi; q += blockDim.x) {
+                const uint32_t loc = (uint32_t)ep.sup_local[q];
+                const V v = *reinterpret_cast<const V*>(tileb + (size_t)apply_cols(pd.fin, K, loc) * sizeof(V));
+                uint64_t gidx = outer;
+                for (int j = 0; j < K; ++j)
+                    if ((loc >> j) & 1u) gidx |= 1ull << pd.sbits[j];
+                const V u = aux[gidx];
+                double* row = ep.pair_sup + (e.rslot * ep.S + ep.sup_pos[q]) * 3;
+                row[0] = norm2(u);
+                row[1] = norm2(v);
+                row[2] = (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+            }
+        } else if (active) {
             V* __restrict__ dst = out + (outer | tg);
 #pragma unroll
             for (int it = 0; it < NA; ++it) {
@@ -392,6 +434,43 @@ __global__ void finalize_dist_kernel(const int64_t* __restrict__ slots, int64_t 
         const double J = block_sum(jsum, sred);
         const double Q = block_sum(qsum, sred);
         if (threadIdx.x == 0) js_out[r] = J + 0.5 * 0.69314718055994530942 * (1.0 - Q);
+    }
+}
+
+// Shift-pair finalisation: one CTA per shifted gate.  With A = sum|Psi0|^2,
+// B = sum|Xi|^2, C = sum Im(Psi0 conj Xi), the two shifted distributions are
+// q+-(s) = (a_s + b_s -+ 2 c_s) / (A + B -+ 2 C)  (psi+- = (Psi0 -+ i Xi)/sqrt2),
+// and each JS loss is formed with the support + remainder identity.
+// slots[2*b] = result slot, slots[2*b+1] = partial slot; out[2r], out[2r+1].
+__global__ void finalize_pair_kernel(const int64_t* __restrict__ slots, int64_t ntiles, const double* __restrict__ partial,
+                                     const double* __restrict__ pair_sup, int64_t S, const double* __restrict__ target,
+                                     double* __restrict__ out) {
+    __shared__ double sred[32];
+    const int64_t r = slots[2 * blockIdx.x], ps = slots[2 * blockIdx.x + 1];
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) {
+        const double* p = partial + (ps * ntiles + i) * 3;
+        a += p[0];
+        b += p[1];
+        c += p[2];
+    }
+    const double A = block_sum(a, sred), B = block_sum(b, sred), C = block_sum(c, sred);
+    const double tp = A + B - 2.0 * C, tm = A + B + 2.0 * C;
+    double jp = 0.0, jm = 0.0, sp = 0.0, sm = 0.0;
+    for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
+        const double* q = pair_sup + (r * S + s) * 3;
+        const double qp = (q[0] + q[1] - 2.0 * q[2]) / tp;
+        const double qm = (q[0] + q[1] + 2.0 * q[2]) / tm;
+        jp += js_term(target[s], qp);
+        jm += js_term(target[s], qm);
+        sp += qp;
+        sm += qm;
+    }
+    const double JP = block_sum(jp, sred), JM = block_sum(jm, sred);
+    const double SP = block_sum(sp, sred), SM = block_sum(sm, sred);
+    if (threadIdx.x == 0) {
+        out[2 * r] = JP + 0.5 * 0.69314718055994530942 * (1.0 - SP);
+        out[2 * r + 1] = JM + 0.5 * 0.69314718055994530942 * (1.0 - SM);
     }
 }
 

@@ -427,22 +427,52 @@ M2 gate_matrix(const Topology& t, int32_t ref, const double* angles) {
 }
 }  // namespace
 
-void circuit_matrices(const Plan& plan, const Topology& topo, const double* angles, double* out) {
-    for (int s = 0; s < plan.n_slots(); ++s) {
-        const FusedOp& op = plan.ops[plan.mat_op[s]];
-        M2 m{cd(1, 0), cd(0, 0), cd(0, 0), cd(1, 0)};
-        bool first = true;
-        for (int32_t ref : op.gates) {
-            const M2 g = gate_matrix(topo, ref, angles);
-            m = first ? g : mul(g, m);
+namespace {
+// Ordered product of a slot's gates; with pauli_gate >= 0 the generator of
+// that rotation (X for RX, Y for RY, Z for RZ) is applied just before it.
+void slot_product(const Plan& plan, const Topology& topo, const double* angles, int s, int32_t pauli_gate,
+                  double* o) {
+    const FusedOp& op = plan.ops[plan.mat_op[s]];
+    M2 m{cd(1, 0), cd(0, 0), cd(0, 0), cd(1, 0)};
+    bool first = true;
+    for (int32_t ref : op.gates) {
+        if (ref >= 0 && ref == pauli_gate) {
+            M2 p;
+            switch (topo.kind[ref]) {
+                case G_RX: p = {cd(0, 0), cd(1, 0), cd(1, 0), cd(0, 0)}; break;
+                case G_RY: p = {cd(0, 0), cd(0, -1), cd(0, 1), cd(0, 0)}; break;
+                case G_RZ: p = {cd(1, 0), cd(0, 0), cd(0, 0), cd(-1, 0)}; break;
+                default: throw std::runtime_error("shifted gate is not a rotation");
+            }
+            m = first ? p : mul(p, m);
             first = false;
         }
-        double* o = out + (size_t)s * 8;
-        o[0] = m.a.real(); o[1] = m.a.imag();
-        o[2] = m.b.real(); o[3] = m.b.imag();
-        o[4] = m.c.real(); o[5] = m.c.imag();
-        o[6] = m.d.real(); o[7] = m.d.imag();
+        const M2 g = gate_matrix(topo, ref, angles);
+        m = first ? g : mul(g, m);
+        first = false;
     }
+    o[0] = m.a.real(); o[1] = m.a.imag();
+    o[2] = m.b.real(); o[3] = m.b.imag();
+    o[4] = m.c.real(); o[5] = m.c.imag();
+    o[6] = m.d.real(); o[7] = m.d.imag();
+}
+}  // namespace
+
+void circuit_matrices(const Plan& plan, const Topology& topo, const double* angles, double* out) {
+    for (int s = 0; s < plan.n_slots(); ++s) slot_product(plan, topo, angles, s, -1, out + (size_t)s * 8);
+}
+
+void slot_matrix_with_pauli(const Plan& plan, const Topology& topo, const double* angles, int slot,
+                            int32_t pauli_gate, double* out8) {
+    slot_product(plan, topo, angles, slot, pauli_gate, out8);
+}
+
+std::vector<int> slot_of_gates(const Plan& plan, const Topology& topo) {
+    std::vector<int> slot(topo.kind.size(), -1);
+    for (int s = 0; s < plan.n_slots(); ++s)
+        for (int32_t ref : plan.ops[plan.mat_op[s]].gates)
+            if (ref >= 0) slot[ref] = s;
+    return slot;
 }
 
 }  // namespace qvb

@@ -130,6 +130,14 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits = 0);
 // `angles` is indexed by topology gate index.
 void circuit_matrices(const Plan& plan, const Topology& topo, const double* angles, double* out);
 
+// Matrix of one slot with the generator Pauli of rotation gate `pauli_gate`
+// (a topology gate index inside that slot) inserted just before the gate.
+void slot_matrix_with_pauli(const Plan& plan, const Topology& topo, const double* angles, int slot,
+                            int32_t pauli_gate, double* out8);
+
+// Slot holding topology gate g (-1 if g is not a one-qubit gate of the plan).
+std::vector<int> slot_of_gates(const Plan& plan, const Topology& topo);
+
 #ifdef __CUDACC__
 #define QV_HD __host__ __device__
 #else

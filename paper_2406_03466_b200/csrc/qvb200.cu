@@ -345,6 +345,42 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     E.stats[11] += (double)nstates * amps * 14.0 * pd.nm;
 }
 
+// Support indices bucketed by the tile of the last pass that holds them
+// (CSR over tiles) with their logical local index inside the tile; sets
+// ep.sup_off / sup_local / sup_pos.  Requires ep.S and ep.ntiles.
+void upload_support_csr(Engine& E, const PassDesc& last, const uint64_t* support, EpiArgs& ep) {
+    const int64_t ntiles = ep.ntiles, S = ep.S;
+    std::vector<int32_t> cnt(ntiles + 1, 0), local(S), tile_of(S);
+    for (int64_t s = 0; s < S; ++s) {
+        const uint64_t g = support[s];
+        uint32_t loc = 0;
+        uint64_t tl = 0;
+        for (int j = 0; j < last.k; ++j)
+            if ((g >> last.sbits[j]) & 1) loc |= 1u << j;
+        for (int j = 0; j < last.n_outer; ++j)
+            if ((g >> last.obits[j]) & 1) tl |= 1ull << j;
+        local[s] = (int32_t)loc;
+        tile_of[s] = (int32_t)tl;
+        cnt[tl + 1]++;
+    }
+    for (int64_t t = 0; t < ntiles; ++t) cnt[t + 1] += cnt[t];
+    std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1), sl(S), sp(S);
+    for (int64_t s = 0; s < S; ++s) {
+        const int32_t at = fill[tile_of[s]]++;
+        sl[at] = local[s];
+        sp[at] = (int32_t)s;
+    }
+    int32_t* doff = E.d_sup_off.get(ntiles + 1);
+    int32_t* dloc = E.d_sup_local.get(S);
+    int32_t* dpos = E.d_sup_pos.get(S);
+    h2d(E, doff, cnt.data(), (ntiles + 1) * 4);
+    h2d(E, dloc, sl.data(), S * 4);
+    h2d(E, dpos, sp.data(), S * 4);
+    ep.sup_off = doff;
+    ep.sup_local = dloc;
+    ep.sup_pos = dpos;
+}
+
 template <typename T>
 void GroupRun::run() {
     typedef typename Cx<T>::V V;
@@ -466,42 +502,8 @@ void GroupRun::run() {
         const int k = plan.k;
         const int64_t ntiles = 1ll << (n - k);
         ep.ntiles = ntiles;
-        // support CSR over the last pass's tiles
-        const PassDesc& last = plan.pdesc[P - 1];
-        if (ep.S > 0) {
-            int pos_of_bit[64];
-            for (int b = 0; b < 64; ++b) pos_of_bit[b] = -1;
-            std::vector<int32_t> cnt(ntiles + 1, 0), local(ep.S), tile_of(ep.S);
-            for (int64_t s = 0; s < ep.S; ++s) {
-                const uint64_t g = R->support[s];
-                uint32_t loc = 0;
-                uint64_t tl = 0;
-                for (int j = 0; j < k; ++j)
-                    if ((g >> last.sbits[j]) & 1) loc |= 1u << j;
-                for (int j = 0; j < last.n_outer; ++j)
-                    if ((g >> last.obits[j]) & 1) tl |= 1ull << j;
-                local[s] = (int32_t)loc;
-                tile_of[s] = (int32_t)tl;
-                cnt[tl + 1]++;
-            }
-            (void)pos_of_bit;
-            for (int64_t t = 0; t < ntiles; ++t) cnt[t + 1] += cnt[t];
-            std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1), sl(ep.S), sp(ep.S);
-            for (int64_t s = 0; s < ep.S; ++s) {
-                const int32_t at = fill[tile_of[s]]++;
-                sl[at] = local[s];
-                sp[at] = (int32_t)s;
-            }
-            int32_t* doff = E.d_sup_off.get(ntiles + 1);
-            int32_t* dloc = E.d_sup_local.get(ep.S);
-            int32_t* dpos = E.d_sup_pos.get(ep.S);
-            h2d(E, doff, cnt.data(), (ntiles + 1) * 4);
-            h2d(E, dloc, sl.data(), ep.S * 4);
-            h2d(E, dpos, sp.data(), ep.S * 4);
-            ep.sup_off = doff;
-            ep.sup_local = dloc;
-            ep.sup_pos = dpos;
-        }
+        (void)k;
+        if (ep.S > 0) upload_support_csr(E, plan.pdesc[P - 1], R->support, ep);
         const bool dist = R->kind == QV_OUT_SUPPORT || R->kind == QV_OUT_JS;
         const bool need_state_out = !dist;   // Pauli / full read the stored state
 
@@ -769,6 +771,185 @@ void execute(Engine& E, const qv_circuits* c, const qv_results* r, double* out, 
     E.stats[5] = ms;
 }
 
+// ---------------------------------------------------------------------------
+// Shift pairs (qv_shift_js): Psi0 once, then one Xi_j per shifted gate, each
+// branching off the unshifted trunk at the pass holding its gate and reduced
+// against Psi0 in its last pass.
+template <typename T>
+void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t nshift, const int64_t* gates,
+                     const qv_results* R, double* out) {
+    typedef typename Cx<T>::V V;
+    const Plan& plan = cp.plan;
+    const Topology& topo = cp.topo;
+    const int n = plan.n, P = (int)plan.pdesc.size();
+    if (plan.single_tile) throw ArgError("shift pairs need a register wider than one tile; use qv_execute");
+    const int slots = plan.n_slots();
+    const size_t slots8 = (size_t)slots * 8;
+    const std::vector<int> slot_of = slot_of_gates(plan, topo);
+    // pass of each slot
+    std::vector<int> pass_of_slot(slots, 0);
+    for (int p = 0; p < P; ++p)
+        for (int s = plan.pdesc[p].m0; s < plan.pdesc[p].m0 + plan.pdesc[p].nm; ++s) pass_of_slot[s] = p;
+
+    // matrix tables: row 0 = base, row 1 + j = base with the Pauli at gate j
+    std::vector<double> base(slots8);
+    circuit_matrices(plan, topo, angles, base.data());
+    std::vector<T> rows((size_t)(nshift + 1) * slots8);
+    for (size_t q = 0; q < slots8; ++q) rows[q] = (T)base[q];
+    std::vector<int> start_pass(nshift);
+    for (int64_t j = 0; j < nshift; ++j) {
+        const int64_t g = gates[j];
+        if (g < 0 || g >= (int64_t)topo.kind.size() || !is_rotation(topo.kind[g]) || slot_of[g] < 0)
+            throw ArgError("gate_index " + std::to_string(g) + " is not a rotation gate of the circuit");
+        double m8[8];
+        slot_matrix_with_pauli(plan, topo, angles, slot_of[g], (int32_t)g, m8);
+        T* row = rows.data() + (size_t)(j + 1) * slots8;
+        for (size_t q = 0; q < slots8; ++q) row[q] = (T)base[q];
+        for (int q = 0; q < 8; ++q) row[(size_t)slot_of[g] * 8 + q] = (T)m8[q];
+        start_pass[j] = pass_of_slot[slot_of[g]];
+    }
+    T* d_mats = reinterpret_cast<T*>(E.d_mats.get(rows.size() * sizeof(T)));
+    h2d(E, d_mats, rows.data(), rows.size() * sizeof(T));
+    auto mats_of = [&](int64_t row) { return (const void*)(d_mats + (size_t)row * slots8); };
+
+    EpiArgs ep;
+    std::memset(&ep, 0, sizeof(ep));
+    ep.n = n;
+    ep.S = R->support_count;
+    ep.ntiles = 1ll << (n - plan.k);
+    const int64_t ntiles = ep.ntiles;
+    uint64_t* dsu = E.d_support.get(std::max<int64_t>(1, ep.S));
+    double* dta = E.d_target.get(std::max<int64_t>(1, ep.S));
+    if (ep.S > 0) {
+        h2d(E, dsu, R->support, ep.S * 8);
+        h2d(E, dta, R->target, ep.S * 8);
+        upload_support_csr(E, plan.pdesc[P - 1], R->support, ep);
+    } else {
+        std::vector<int32_t> zeros(ntiles + 1, 0);
+        int32_t* doff = E.d_sup_off.get(ntiles + 1);
+        h2d(E, doff, zeros.data(), zeros.size() * 4);
+        ep.sup_off = doff;
+    }
+    ep.support = dsu;
+    ep.target = dta;
+    ep.pair_sup = E.d_pauli_out.get((size_t)std::max<int64_t>(1, nshift * ep.S * 3));
+    double* d_out = E.d_js_out.get((size_t)2 * nshift);
+
+    // memory: Psi0 + trunk + W work states
+    const size_t state_bytes = sizeof(V) << n;
+    const uint64_t avail = E.budget / state_bytes;
+    if (avail < 3) throw ArgError("shift pairs need three " + std::to_string(n) + "-qubit states in the memory budget");
+    const int64_t W = std::max<int64_t>(1, std::min<int64_t>({(int64_t)avail - 2, (int64_t)64, nshift}));
+    unsigned char* base_ptr = E.d_states.get((size_t)(W + 2) * state_bytes);
+    V* psi0 = reinterpret_cast<V*>(base_ptr);
+    V* trunk = reinterpret_cast<V*>(base_ptr + state_bytes);
+    auto work = [&](int64_t b) { return reinterpret_cast<V*>(base_ptr + (size_t)(2 + b) * state_bytes); };
+    double* partial = E.d_partial.get((size_t)W * ntiles * 3);
+
+    // ---- schedule ----------------------------------------------------------
+    struct L { bool pass; int p; size_t off; int count; int flags; double bytes; };
+    std::vector<L> sched;
+    std::vector<LaunchEntry> ents;
+    std::vector<int64_t> slots_tab;
+    for (int p = 0; p < P; ++p) {   // phase 1: Psi0
+        ents.push_back({p == 0 ? nullptr : (const void*)psi0, (void*)psi0, mats_of(0), 0, 0, nullptr});
+        sched.push_back({true, p, ents.size() - 1, 1, F_STORE, (double)state_bytes * ((p ? 1 : 0) + 1)});
+    }
+    std::vector<std::vector<int64_t>> by_pass(P);
+    for (int64_t j = 0; j < nshift; ++j) by_pass[start_pass[j]].push_back(j);
+    int last_needed = -1;
+    for (int p = 0; p < P; ++p)
+        if (!by_pass[p].empty()) last_needed = p;
+    for (int p = 0; p <= last_needed; ++p) {   // phase 2: branches off the trunk
+        const auto& D = by_pass[p];
+        for (size_t b0 = 0; b0 < D.size(); b0 += (size_t)W) {
+            const int nb = (int)std::min<size_t>((size_t)W, D.size() - b0);
+            for (int pp = p; pp < P; ++pp) {
+                const bool lastp = pp == P - 1;
+                const size_t off = ents.size();
+                for (int b = 0; b < nb; ++b) {
+                    const void* in = pp == p ? (p == 0 ? nullptr : (const void*)trunk) : (const void*)work(b);
+                    ents.push_back({in, lastp ? nullptr : (void*)work(b), mats_of(1 + D[b0 + b]), D[b0 + b], b,
+                                    (const void*)psi0});
+                }
+                const double rd = (pp == p && p == 0) ? 0.0 : 1.0;
+                sched.push_back({true, pp, off, nb, lastp ? F_PAIR : F_STORE,
+                                 nb * (double)state_bytes * (lastp ? 2.0 : rd + 1.0)});
+            }
+            const size_t off = slots_tab.size();
+            for (int b = 0; b < nb; ++b) { slots_tab.push_back(D[b0 + b]); slots_tab.push_back(b); }
+            sched.push_back({false, 0, off, nb, 0, 0});
+        }
+        if (p < last_needed) {   // advance the trunk by pass p
+            ents.push_back({p == 0 ? nullptr : (const void*)trunk, (void*)trunk, mats_of(0), 0, 0, nullptr});
+            sched.push_back({true, p, ents.size() - 1, 1, F_STORE, (double)state_bytes * ((p ? 1 : 0) + 1)});
+        }
+    }
+    LaunchEntry* dent = E.d_entries.get(ents.size());
+    h2d(E, dent, ents.data(), ents.size() * sizeof(LaunchEntry));
+    int64_t* dslots = E.d_slots.get(std::max<size_t>(2, slots_tab.size()));
+    if (!slots_tab.empty()) h2d(E, dslots, slots_tab.data(), slots_tab.size() * 8);
+    cudaEvent_t call0 = E.next_event();
+    CK(cudaEventRecord(call0, E.stream));
+    for (const L& l : sched) {
+        if (l.pass) {
+            EpiArgs e2 = ep;
+            e2.flags = l.flags;
+            e2.partial = partial;
+            launch_pass<T>(E, plan.pdesc[l.p], cp.d_groups.p, dent + l.off, l.count, ntiles, e2, l.p == 0);
+            E.stats[1] += l.count;
+            E.stats[4] += l.bytes;
+        } else {
+            finalize_pair_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, ntiles, partial, ep.pair_sup, ep.S,
+                                                                 ep.target, d_out);
+            CK(cudaGetLastError());
+            E.stats[0] += 1;
+        }
+    }
+    cudaEvent_t call1 = E.next_event();
+    CK(cudaEventRecord(call1, E.stream));
+    d2h(E, out, d_out, (size_t)2 * nshift * 8);
+    float call_ms = 0.f;
+    CK(cudaEventElapsedTime(&call_ms, call0, call1));
+    E.stats[8] += call_ms;
+    E.stats[2] += (double)2 * nshift * P;   // sweeps of direct, unshared simulation of the 2n circuits
+    E.stats[3] += (double)nshift + 1;
+    E.stats[6] = P;
+    E.stats[7] = plan.k;
+}
+
+void shift_js(Engine& E, const qv_circuits* c, int64_t nshift, const int64_t* gates, const qv_results* r, double* out) {
+    if (!c || !gates || !r || !out) throw ArgError("null argument");
+    if (c->n_circuits != 1) throw ArgError("shift pairs take exactly one base circuit");
+    if (r->kind != QV_OUT_JS) throw ArgError("shift pairs return JS losses (results->kind = QV_OUT_JS)");
+    if (nshift < 1) throw ArgError("no gates to shift");
+    Request q{c, r, c->n_qubits, 1};
+    validate(q);
+    CK(cudaSetDevice(E.device));
+    std::memset(E.stats, 0, sizeof(E.stats));
+    E.events_used = 0;
+    E.timed.clear();
+    Topology t;
+    t.n = c->n_qubits;
+    const int64_t g0 = c->uniform ? 0 : c->gate_offsets[0];
+    const int64_t g1 = c->uniform ? c->n_gates : c->gate_offsets[1];
+    t.kind.assign(c->kinds + g0, c->kinds + g1);
+    t.q0.assign(c->q0 + g0, c->q0 + g1);
+    t.q1.assign(c->q1 + g0, c->q1 + g1);
+    for (size_t g = 0; g < t.kind.size(); ++g)
+        if (!is_two_qubit(t.kind[g])) t.q1[g] = -1;
+    CachedPlan& cp = get_plan(E, std::move(t));
+    if (E.precision == 0) run_shift_pairs<double>(E, cp, c->angles + g0, nshift, gates, r, out);
+    else run_shift_pairs<float>(E, cp, c->angles + g0, nshift, gates, r, out);
+    double ms = 0;
+    for (auto& pr : E.timed) {
+        float x = 0.f;
+        CK(cudaEventElapsedTime(&x, pr.first, pr.second));
+        ms += x;
+    }
+    E.stats[5] = ms;
+}
+
 }  // namespace qvb
 
 // ---------------------------------------------------------------------------
@@ -842,6 +1023,32 @@ int qv_execute(qv_handle h, const qv_circuits* circuits, const qv_results* resul
     E->err_circuit = -1;
     try {
         execute(*E, circuits, results, out, out_len);
+        return QV_OK;
+    } catch (const CircuitError& e) {
+        E->err = e.what();
+        E->err_circuit = e.index;
+        return QV_ERR_CIRCUIT;
+    } catch (const ArgError& e) {
+        E->err = e.what();
+        return QV_ERR_ARGUMENT;
+    } catch (const CudaError& e) {
+        E->err = e.what();
+        return QV_ERR_CUDA;
+    } catch (const std::exception& e) {
+        E->err = e.what();
+        return QV_ERR_INTERNAL;
+    }
+}
+
+int qv_shift_js(qv_handle h, const qv_circuits* base, int64_t n_shift, const int64_t* gate_index,
+                const qv_results* results, double* out) {
+    if (!h) return QV_ERR_ARGUMENT;
+    Engine* E = reinterpret_cast<Engine*>(h);
+    std::lock_guard<std::mutex> lk(E->mu);
+    E->err.clear();
+    E->err_circuit = -1;
+    try {
+        shift_js(*E, base, n_shift, gate_index, results, out);
         return QV_OK;
     } catch (const CircuitError& e) {
         E->err = e.what();

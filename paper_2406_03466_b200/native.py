@@ -27,7 +27,7 @@ QV_OUT_PAULI, QV_OUT_SUPPORT, QV_OUT_FULL, QV_OUT_JS = range(4)
 PRECISIONS = {"complex128": QV_COMPLEX128, "complex64": QV_COMPLEX64}
 
 # Symbols include/qvb200.h declares (checked by the CPU test suite).
-EXPORTS = ("qv_version", "qv_output_size", "qv_create", "qv_destroy", "qv_execute",
+EXPORTS = ("qv_version", "qv_output_size", "qv_create", "qv_destroy", "qv_execute", "qv_shift_js",
            "qv_last_error", "qv_last_error_circuit", "qv_last_stats", "qv_device_count")
 
 STAT_NAMES = ("launches", "sweeps", "sweeps_unshared", "unique_states", "pass_bytes",
@@ -88,6 +88,9 @@ def load_library() -> ctypes.CDLL:
             lib.qv_last_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
             lib.qv_device_count.restype = ctypes.c_int
             lib.qv_device_count.argtypes = []
+            lib.qv_shift_js.restype = ctypes.c_int
+            lib.qv_shift_js.argtypes = [ctypes.c_void_p, ctypes.POINTER(QvCircuits), ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.POINTER(QvResults), ctypes.c_void_p]
             _lib = lib
         return _lib
 
@@ -159,13 +162,40 @@ class Engine:
             raise ValueError("malformed result request")
         out = np.empty(max(int(size), 1), dtype=np.float64)
         code = self._lib.qv_execute(self._handle, ctypes.byref(c), ctypes.byref(r), out.ctypes.data, out.shape[0])
+        self._finish(code)
+        return out[:size]
+
+    def shift_js(self, n_qubits: int, base: "LoweredBatch", gate_index: np.ndarray, support: np.ndarray,
+                 target: np.ndarray) -> np.ndarray:
+        """qv_shift_js: JS losses at t_g +- pi/2 for each rotation gate g of one
+        bound circuit; returns [2 * len(gate_index)] ('+' then '-' per gate)."""
+        c = QvCircuits()
+        c.n_qubits = n_qubits
+        c.n_circuits = 1
+        c.uniform = 1
+        c.n_gates = base.n_gates
+        c.kinds, c.q0, c.q1, c.angles = (_ptr(base.kinds), _ptr(base.q0), _ptr(base.q1), _ptr(base.angles))
+        gates = np.ascontiguousarray(gate_index, dtype=np.int64)
+        support = np.ascontiguousarray(support, dtype=np.uint64)
+        target = np.ascontiguousarray(target, dtype=np.float64)
+        r = QvResults()
+        r.kind = QV_OUT_JS
+        r.support_count = support.shape[0]
+        r.support = _ptr(support)
+        r.target = _ptr(target)
+        out = np.empty(2 * gates.shape[0], dtype=np.float64)
+        code = self._lib.qv_shift_js(self._handle, ctypes.byref(c), gates.shape[0], gates.ctypes.data,
+                                     ctypes.byref(r), out.ctypes.data)
+        self._finish(code)
+        return out
+
+    def _finish(self, code: int) -> None:
         stats = np.zeros(len(STAT_NAMES), dtype=np.float64)
         self._lib.qv_last_stats(self._handle, stats.ctypes.data, stats.shape[0])
         self.last_stats = dict(zip(STAT_NAMES, stats.tolist()))
         if code != QV_OK:
             msg = (self._lib.qv_last_error(self._handle) or b"").decode()
             raise NativeError(code, msg, int(self._lib.qv_last_error_circuit(self._handle)))
-        return out[:size]
 
 
 class LoweredBatch:

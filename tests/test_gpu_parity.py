@@ -134,6 +134,38 @@ def test_qcl_full_gradient_multi_tile(gpu, golden_large, idx):
     assert np.max(np.abs(np.array(rep.gradient) - case["gradient"])) < TOL128
 
 
+def test_shift_pairs_match_reference_and_direct(gpu, golden_large):
+    """qv_shift_js (Psi0 -+ i Xi forms) against the reference's losses of the
+    directly shifted circuits, and against direct simulation on the GPU."""
+    backend = qv.B200Backend(device=0)
+    for case in golden_large["qcl_forward"]:
+        n, layers = case["n"], case["layers"]
+        if n <= 12 or not case["shifted"]:
+            continue
+        theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), case["theta_seed"])
+        target = qv.random_target_distribution(n, case["target_seed"])
+        tpl = qv.ddcl_circuit_template(n, layers)
+        ks = sorted({s["k"] for s in case["shifted"]})
+        losses = backend.shift_js_losses(tpl, theta, target, ks)
+        for s in case["shifted"]:
+            got = losses[2 * ks.index(s["k"]) + (0 if s["tag"] == "+" else 1)]
+            assert got == pytest.approx(s["js"], abs=TOL128), (n, s)
+    case = golden_large["qcl_gradient"][0]   # 14 qubits x 1 layer, every parameter
+    n, layers = case["n"], case["layers"]
+    theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), case["theta_seed"])
+    target = qv.random_target_distribution(n, case["target_seed"])
+    pair = backend.shift_js_losses(qv.ddcl_circuit_template(n, layers), theta, target, list(range(len(theta))))
+    assert np.max(np.abs(pair - case["losses"])) < TOL128
+    direct = backend.js_losses(qv.ddcl_batch(qv.DdclSpec(n, layers, theta, target)), n, target)
+    assert np.max(np.abs(pair - direct)) < 1e-13
+    rep_pair = qv.ddcl_gradient(qv.DdclSpec(n, layers, theta, target), qv.VqpuPoolConfig(n_virtual_qpus=3))
+    rep_direct = qv.ddcl_gradient(qv.DdclSpec(n, layers, theta, target), qv.VqpuPoolConfig(), shift_mode="direct")
+    assert np.max(np.abs(np.array(rep_pair.gradient) - case["gradient"])) < TOL128
+    assert np.max(np.abs(np.array(rep_direct.gradient) - case["gradient"])) < TOL128
+    with pytest.raises(qv.ExecutionError):   # one tile: use js_losses
+        backend.shift_js_losses(qv.ddcl_circuit_template(4, 1), [0.1] * 24, qv.random_target_distribution(4, 1), [0])
+
+
 def test_complex64_within_1e5(gpu, golden_small, golden_large):
     cfg = golden_small["qcl_config1"]
     n, layers = cfg["n"], cfg["layers"]
