@@ -20,11 +20,11 @@ namespace qvb {
 constexpr int kRegBits = 4;          // max register bits per group (descriptor capacity)
 constexpr int kGroupAmps = 1 << kRegBits;
 
-// Register bits per group (amplitudes per thread = 2^R).  complex128 uses 3
-// (8 amplitudes, ~100 registers) so a 4096-amplitude tile runs on 512 threads
-// = 16 warps per SM: FP64 latency (8 cycles, one DFMA per ~2.3 cycles per
-// warp, measured) needs >= 2 warps per scheduler in their math phase.
-// complex64 uses 4 (16 amplitudes) over 8192-amplitude tiles.
+// Register bits per group (amplitudes per thread = 2^R).  4 for both
+// precisions: 16 amplitudes and up to four 2x2 matrices per shared-memory
+// round trip.  (Measured on B200: R = 3 at complex128 -- 512 threads per tile,
+// twice the warps -- was 20% slower than R = 4 because every group then pays
+// its round trip for only three matrices.)
 #ifndef QV_C128_REG_BITS
 #define QV_C128_REG_BITS 4
 #endif

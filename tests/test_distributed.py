@@ -1,0 +1,61 @@
+"""Multi-process path of the virtual-QPU pool on CPU (torch.distributed,
+gloo, world size 2): block b runs on rank b mod W, per-circuit scalars are
+exchanged with one padded all-gather, every rank ends with the full vector
+in batch order.  A stub backend stands in for the GPU (the exchange logic is
+what is under test; the B200 path runs the same code with NCCL)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2406_03466_b200 as qv
+
+
+class StubBackend:
+    """Deterministic per-circuit value: a function of the circuit alone."""
+
+    executed: list = []
+
+    def values(self, block):
+        return np.array([float(c.name[1:]) * 1.5 + 0.25 for c in block])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n_circuits, n_vqpus, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        batch = [qv.Circuit(2, (qv.h(0),), name=f"c{i}") for i in range(n_circuits)]
+        seen = []
+
+        def evaluate(backend, block):
+            seen.extend(c.name for c in block)
+            return backend.values(block)
+
+        _, values = qv.execute_values(batch, 2, qv.VqpuPoolConfig(n_virtual_qpus=n_vqpus), StubBackend, evaluate)
+        out[rank] = (values.tolist(), seen)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_circuits,n_vqpus", [(10, 4), (7, 16), (2688, 16), (5, 1)])
+def test_execute_values_two_ranks(n_circuits, n_vqpus):
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_worker, args=(2, _free_port(), n_circuits, n_vqpus, out), nprocs=2, join=True)
+    want = [i * 1.5 + 0.25 for i in range(n_circuits)]
+    blocks = [b for b in qv.partition(n_circuits, n_vqpus) if b.size]
+    for rank in range(2):
+        values, seen = out[rank]
+        assert values == want
+        mine = [f"c{i}" for j, b in enumerate(blocks) if j % 2 == rank for i in range(b.start, b.end)]
+        assert seen == mine
