@@ -243,10 +243,20 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         }
         // ---- register groups --------------------------------------------------
         if (!zero_tile) {
+            // the tile buffer's byte offset (a multiple of 2^16 > every slot
+            // offset) is folded into the XOR base: one address op per amplitude
+            const uint32_t boff = (uint32_t)(tileb - smem_raw);
             for (int g = 0; g < pd.ng; ++g) {
                 if (active) {
                     const GroupDesc& G = sg[g];
-                    uint32_t base = 0;
+                    const int4 mats = *reinterpret_cast<const int4*>(G.mat);
+                    // first matrix in flight before the amplitudes
+                    V m00, m01, m10, m11;
+                    if (mats.x >= 0) {
+                        const V* M = smat + mats.x * 4;
+                        m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
+                    }
+                    uint32_t base = boff;
 #pragma unroll
                     for (int m = 0; m < TB; ++m)
                         if ((tid >> m) & 1) base ^= G.tcol[m];
@@ -259,16 +269,17 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
                         off[4 * q + 2] = base ^ c.z;
                         off[4 * q + 3] = base ^ c.w;
                     }
-                    const int4 mats = *reinterpret_cast<const int4*>(G.mat);
                     V a[NA];
 #pragma unroll
-                    for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(tileb + off[j]);
+                    for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off[j]);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
                         if (mi >= 0) {
-                            const V* M = smat + mi * 4;
-                            const V m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
+                            if (r > 0) {
+                                const V* M = smat + mi * 4;
+                                m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
+                            }
 #pragma unroll
                             for (int j = 0; j < NA; ++j)
                                 if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
@@ -276,7 +287,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
                     }
                     if (g < 29) QV_MARK(2 + 2 * g);
 #pragma unroll
-                    for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(tileb + off[j]) = a[j];
+                    for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off[j]) = a[j];
                 }
                 // warp-local segment: the next group reads only what this warp wrote
                 if (g + 1 < pd.ng && !sg[g + 1].cta_sync) __syncwarp();
