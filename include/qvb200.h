@@ -61,6 +61,9 @@ extern "C" {
 #define QV_OUT_FULL 2       /* per circuit: all 2^n normalised probabilities (n <= 24)          */
 #define QV_OUT_JS 3         /* per circuit: JS(target || p) via the support+remainder identity  */
                             /* (ddcl.py:37-61 over born_distribution)                            */
+#define QV_OUT_COUNTS 4     /* per circuit: `shots` samples of the outcome distribution with the  */
+                            /* reference's sampler (backend.py:234-251): numpy PCG64 doubles,     */
+                            /* inverse CDF on the sequential cumsum, side="right" (n <= 24)       */
 
 typedef struct qv_engine* qv_handle;
 
@@ -101,13 +104,20 @@ typedef struct qv_results {
     int64_t support_count;
     const uint64_t* support;
     const double* target;
+    /* QV_OUT_COUNTS: shots per circuit, and each circuit's PCG64 generator
+     * state as numpy's PCG64(seed).state holds it: rng_state[4c + 0..3] =
+     * (state >> 64, state & (2^64-1), inc >> 64, inc & (2^64-1)).           */
+    int64_t shots;
+    const uint64_t* rng_state;
 } qv_results;
 
 /* Output sizes (doubles) written to `out`:
  *   PAULI   : term_offsets[n_circuits]                     (term t of circuit c at term_offsets[c]+t)
  *   SUPPORT : n_circuits * (support_count + 1)             (row: p_0..p_{S-1}, norm)
  *   FULL    : n_circuits * 2^n_qubits
- *   JS      : n_circuits                                                              */
+ *   JS      : n_circuits
+ *   COUNTS  : n_circuits * (2 * shots + 1); row: m, then m (outcome index, count)
+ *             pairs in ascending index order                                          */
 int64_t qv_output_size(const qv_circuits* circuits, const qv_results* results);
 
 /* Create an executor bound to CUDA device `device`.  `memory_budget_bytes`

@@ -32,7 +32,7 @@ from typing import Iterable, Mapping, Protocol, Sequence
 import numpy as np
 
 from . import native
-from .ir import CODE_BY_VALUE, Circuit, bind
+from .ir import CODE_BY_VALUE, Circuit, bind, h, measure_all
 from .observables import Observable, PauliTerm, term_masks
 from .results import ChildResult, ResultBuffer
 
@@ -207,17 +207,16 @@ class B200Backend:
     # -- Accelerator -------------------------------------------------------
     def execute(self, buffer: ResultBuffer, circuits: Sequence[Circuit], config: ExecutionConfig) -> None:
         n = buffer.n_qubits
+        counts = config.mode == "counts"
         stop, reason = len(circuits), ""
         for i, c in enumerate(circuits):
-            reason = self._precheck(c, n)
+            reason = self._precheck(c, n, children=not counts) or (self._counts_precheck(c, n) if counts else "")
             if reason:
                 stop = i
                 break
         ok = circuits[:stop]
         if ok:
-            if config.mode != "expectation":
-                raise ExecutionError(ok[0].name, "counts mode is not implemented by the B200 backend")
-            children = self._children(ok, n)
+            children = self._counts_children(ok, n, config) if config.mode == "counts" else self._children(ok, n)
             if hasattr(buffer, "extend_children"):
                 buffer.extend_children(children)
             else:   # a reference `qvirt.ResultBuffer`
@@ -298,6 +297,55 @@ class B200Backend:
             return (f"a full {n}-qubit distribution has 2^{n} entries; construct the backend "
                     "with support= to receive the target support plus the remainder")
         return ""
+
+    @staticmethod
+    def _counts_precheck(c, n: int) -> str:
+        """Counts-mode rules of reference backend.py:314-317, pauli.py:147-162."""
+        obs = c.observable
+        if n > MAX_FULL_DISTRIBUTION_QUBITS:
+            return f"counts mode samples a 2^{n} distribution; limited to {MAX_FULL_DISTRIBUTION_QUBITS} qubits"
+        if obs is None:
+            return ""
+        if hasattr(obs, "terms"):
+            return "counts mode measures one Pauli term per circuit"
+        if any(letter == "Y" for _, letter in obs.factors):
+            return "no basis-change gates for Y factors"
+        return ""
+
+    def _counts_children(self, circuits, n, config: ExecutionConfig) -> list[ChildResult]:
+        """Sample `config.shots` outcomes per circuit on the device with the
+        reference's sampler: seed = config.seed + first_global_index + offset
+        (backend.py:297, :320), PCG64 doubles, inverse CDF (backend.py:234-251).
+        Circuits with a Pauli term are first rotated into its basis (H on each
+        X factor; pauli.py:147-162)."""
+        from types import SimpleNamespace
+
+        mask64 = (1 << 64) - 1
+        states = np.zeros((len(circuits), 4), dtype=np.uint64)
+        for off in range(len(circuits)):
+            st = np.random.PCG64(config.seed + config.first_global_index + off).state["state"]
+            s, inc = int(st["state"]), int(st["inc"])
+            states[off] = (s >> 64, s & mask64, inc >> 64, inc & mask64)
+        runs = []
+        for c in circuits:
+            gates = tuple(c.gates)
+            if c.observable is not None:
+                gates = gates + tuple(h(q) for q, letter in c.observable.factors if letter == "X") + (measure_all(),)
+            runs.append(SimpleNamespace(gates=gates, name=c.name, n_qubits=n, observable=None))
+        lowered = lower_batch(runs)
+        shots = int(config.shots)
+        out = self._run(lowered, n, native.QV_OUT_COUNTS, circuits, shots=shots, rng_state=states)
+        rows = out.reshape(len(circuits), 2 * shots + 1)
+        fmt = f"0{n}b"
+        children = []
+        for c, row in zip(circuits, rows):
+            m = int(row[0])
+            idx = row[1:1 + 2 * m:2].astype(np.int64)
+            cnt = row[2:2 + 2 * m:2].astype(np.int64)
+            counts = {format(int(i), fmt): int(k) for i, k in zip(idx, cnt)}
+            children.append(ChildResult(name=c.name, counts=counts, shots=shots))
+        self.gate_counter += sum(len(r.gates) for r in runs)
+        return children
 
     def _check_all(self, circuits, n):
         for c in circuits:

@@ -26,7 +26,8 @@ PRODUCT = PKG / "libqvb200.so"
 PLANCHECK = PKG / "libqvb200_plan.so"
 
 PRODUCT_SOURCES = [CSRC / "qvb200.cu", CSRC / "plan.cpp"]
-PRODUCT_DEPS = PRODUCT_SOURCES + [CSRC / "kernels.cuh", CSRC / "plan.hpp", INCLUDE / "qvb200.h"]
+PRODUCT_DEPS = PRODUCT_SOURCES + [CSRC / "kernels.cuh", CSRC / "sampling.cuh", CSRC / "plan.hpp",
+                                  INCLUDE / "qvb200.h"]
 PLANCHECK_SOURCES = [CSRC / "plancheck.cpp", CSRC / "plan.cpp"]
 PLANCHECK_DEPS = PLANCHECK_SOURCES + [CSRC / "plan.hpp"]
 

@@ -32,6 +32,7 @@
 
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "sampling.cuh"
 #include "qvb200.h"
 
 namespace qvb {
@@ -180,7 +181,7 @@ void validate(const Request& q) {
         }
     }
     const qv_results* r = q.r;
-    if (r->kind < QV_OUT_PAULI || r->kind > QV_OUT_JS) throw ArgError("unknown result kind");
+    if (r->kind < QV_OUT_PAULI || r->kind > QV_OUT_COUNTS) throw ArgError("unknown result kind");
     const uint64_t full = n >= 64 ? ~0ull : ((1ull << n) - 1);
     if (r->kind == QV_OUT_PAULI) {
         if (!r->term_offsets || !r->xmask || !r->ymask || !r->zmask) throw ArgError("null Pauli arrays");
@@ -202,6 +203,10 @@ void validate(const Request& q) {
         }
     } else if (r->kind == QV_OUT_FULL) {
         if (n > 24) throw ArgError("full distributions are limited to 24 qubits");
+    } else if (r->kind == QV_OUT_COUNTS) {
+        if (n > 24) throw ArgError("counts mode is limited to 24 qubits");
+        if (r->shots < 1) throw ArgError("shots must be positive");
+        if (!r->rng_state) throw ArgError("counts mode needs one PCG64 state per circuit");
     }
 }
 
@@ -211,6 +216,7 @@ int64_t output_size(const qv_circuits* c, const qv_results* r) {
         case QV_OUT_SUPPORT: return (int64_t)c->n_circuits * (r->support_count + 1);
         case QV_OUT_FULL: return (int64_t)c->n_circuits << c->n_qubits;
         case QV_OUT_JS: return c->n_circuits;
+        case QV_OUT_COUNTS: return r->shots > 0 ? (int64_t)c->n_circuits * (2 * r->shots + 1) : -1;
         default: return -1;
     }
 }
@@ -476,7 +482,9 @@ void GroupRun::run() {
     }
     ep.sup_out = E.d_sup_out.get((size_t)U * (ep.S + 1));
     ep.js_out = E.d_js_out.get(U);
-    if (R->kind == QV_OUT_FULL) ep.full_out = E.d_full_out.get((size_t)U << n);
+    // full distributions (FULL) and the CDF rows counts mode samples from (COUNTS)
+    const bool probs = R->kind == QV_OUT_FULL || R->kind == QV_OUT_COUNTS;
+    if (probs) ep.full_out = E.d_full_out.get((size_t)U << n);
 
     const size_t state_bytes = sizeof(V) << n;
     cudaEvent_t call0 = E.next_event();
@@ -492,7 +500,7 @@ void GroupRun::run() {
         if (R->kind == QV_OUT_PAULI) ep.flags |= F_S_PAULI;
         if (R->kind == QV_OUT_SUPPORT) ep.flags |= F_S_SUPPORT;
         if (R->kind == QV_OUT_JS) ep.flags |= F_S_JS;
-        if (R->kind == QV_OUT_FULL) ep.flags |= F_S_FULL;
+        if (probs) ep.flags |= F_S_FULL;
         ep.ntiles = 1;
         if (U > 0x7fffffffll) throw ArgError("batch too large");
         launch_pass<T>(E, plan.pdesc[0], cp.d_groups.p, dent, (int)U, 1, ep, false);
@@ -562,15 +570,15 @@ void GroupRun::run() {
                     }
                     int flags = F_STORE;
                     if (lastp && dist) flags = F_NORM | F_SUPPORT;
-                    if (lastp && R->kind == QV_OUT_FULL) flags = F_STORE | F_NORM;
+                    if (lastp && probs) flags = F_STORE | F_NORM;
                     const double rd = (pp == p && p == 0) ? 0.0 : 1.0, wr = (flags & F_STORE) ? 1.0 : 0.0;
                     sched.push_back({L_PASS, pp, off, nb, flags, nullptr, 0, 0, nb * (double)state_bytes * (rd + wr)});
                 }
-                if (dist || R->kind == QV_OUT_FULL) {
+                if (dist || probs) {
                     const size_t off = slots_tab.size();
                     for (int b = 0; b < nb; ++b) { slots_tab.push_back(D[b0 + b]); slots_tab.push_back(b); }
                     sched.push_back({L_FINAL_DIST, 0, off, nb, 0, nullptr, 0, 0, 0});
-                    if (R->kind == QV_OUT_FULL)
+                    if (probs)
                         for (int b = 0; b < nb; ++b) sched.push_back({L_FULL, 0, 0, 1, 0, work(b), D[b0 + b], 0, 0});
                 } else {
                     for (int b = 0; b < nb; ++b) {
@@ -658,6 +666,37 @@ void GroupRun::run() {
         if (!alive.empty()) throw std::runtime_error("scheduler left states unfinished");
         E.stats[2] += (double)C * P;
     }
+    // counts mode: CDF rows (sequential cumsum, numpy order), then per circuit
+    // PCG64 draws -> integer histogram -> ascending (index, count) pairs
+    double* d_counts = nullptr;
+    const int64_t row_len = R->kind == QV_OUT_COUNTS ? 2 * R->shots + 1 : 0;
+    if (R->kind == QV_OUT_COUNTS) {
+        const int64_t dim = 1ll << n;
+        cumsum_kernel<<<(unsigned)((U + 127) / 128), 128, 0, E.stream>>>(ep.full_out, dim, U);
+        CK(cudaGetLastError());
+        std::vector<int64_t> erow(C);
+        std::vector<uint64_t> rng((size_t)C * 4);
+        for (int64_t i = 0; i < C; ++i) {
+            erow[i] = uniq_of[i];
+            std::memcpy(rng.data() + 4 * i, R->rng_state + 4 * circuits[i], 4 * sizeof(uint64_t));
+        }
+        int64_t* d_erow = E.d_slots.get(std::max<int64_t>(2, C));
+        h2d(E, d_erow, erow.data(), C * 8);
+        uint64_t* d_rng = E.d_support.get(4 * C);
+        h2d(E, d_rng, rng.data(), rng.size() * 8);
+        d_counts = E.d_pauli_out.get((size_t)C * row_len);
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(C, (int64_t)(1ll << 30) / (dim * 4)));
+        unsigned* hist = reinterpret_cast<unsigned*>(E.d_partial2.get((size_t)(chunk * dim * 4 + 15) / 16));
+        for (int64_t c0 = 0; c0 < C; c0 += chunk) {
+            const int64_t cc = std::min(chunk, C - c0);
+            CK(cudaMemsetAsync(hist, 0, (size_t)cc * dim * 4, E.stream));
+            sample_kernel<<<(unsigned)cc, 256, 0, E.stream>>>(ep.full_out, d_erow, d_rng, R->shots, dim, hist, c0);
+            CK(cudaGetLastError());
+            compact_counts_kernel<<<(unsigned)cc, 1024, 0, E.stream>>>(hist, dim, d_counts, row_len, c0);
+            CK(cudaGetLastError());
+            E.stats[0] += 2;
+        }
+    }
     cudaEvent_t call1 = E.next_event();
     CK(cudaEventRecord(call1, E.stream));
 
@@ -680,6 +719,11 @@ void GroupRun::run() {
         std::vector<double> vals(U);
         d2h(E, vals.data(), ep.js_out, U * 8);
         for (int64_t i = 0; i < C; ++i) out[circuits[i]] = vals[uniq_of[i]];
+    } else if (R->kind == QV_OUT_COUNTS) {
+        std::vector<double> vals((size_t)C * row_len);
+        d2h(E, vals.data(), d_counts, vals.size() * 8);
+        for (int64_t i = 0; i < C; ++i)
+            std::memcpy(out + (size_t)circuits[i] * row_len, vals.data() + (size_t)i * row_len, row_len * 8);
     } else {
         const size_t row = (size_t)1 << n;
         std::vector<double> vals((size_t)U * row);

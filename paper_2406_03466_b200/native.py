@@ -22,7 +22,7 @@ LIB_PATH = Path(os.environ.get("QVB200_LIB", Path(__file__).resolve().parent / "
 
 QV_OK, QV_ERR_ARGUMENT, QV_ERR_CIRCUIT, QV_ERR_CUDA, QV_ERR_INTERNAL = range(5)
 QV_COMPLEX128, QV_COMPLEX64 = 0, 1
-QV_OUT_PAULI, QV_OUT_SUPPORT, QV_OUT_FULL, QV_OUT_JS = range(4)
+QV_OUT_PAULI, QV_OUT_SUPPORT, QV_OUT_FULL, QV_OUT_JS, QV_OUT_COUNTS = range(5)
 
 PRECISIONS = {"complex128": QV_COMPLEX128, "complex64": QV_COMPLEX64}
 
@@ -56,7 +56,8 @@ class QvCircuits(ctypes.Structure):
 class QvResults(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("term_offsets", ctypes.c_void_p),
                 ("xmask", ctypes.c_void_p), ("ymask", ctypes.c_void_p), ("zmask", ctypes.c_void_p),
-                ("support_count", ctypes.c_int64), ("support", ctypes.c_void_p), ("target", ctypes.c_void_p)]
+                ("support_count", ctypes.c_int64), ("support", ctypes.c_void_p), ("target", ctypes.c_void_p),
+                ("shots", ctypes.c_int64), ("rng_state", ctypes.c_void_p)]
 
 
 _lib = None
@@ -129,7 +130,8 @@ class Engine:
 
     def execute(self, n_qubits: int, lowered: "LoweredBatch", result_kind: int, *,
                 terms: tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray] | None = None,
-                support: np.ndarray | None = None, target: np.ndarray | None = None) -> np.ndarray:
+                support: np.ndarray | None = None, target: np.ndarray | None = None,
+                shots: int = 0, rng_state: np.ndarray | None = None) -> np.ndarray:
         """Run one batch; returns the flat float64 output (layout: qvb200.h)."""
         c = QvCircuits()
         c.n_qubits = n_qubits
@@ -157,6 +159,11 @@ class Engine:
             target = np.ascontiguousarray(target, dtype=np.float64)
             keep.append(target)
             r.target = _ptr(target)
+        if rng_state is not None:
+            rng_state = np.ascontiguousarray(rng_state, dtype=np.uint64)
+            keep.append(rng_state)
+            r.rng_state = _ptr(rng_state)
+            r.shots = int(shots)
         size = self._lib.qv_output_size(ctypes.byref(c), ctypes.byref(r))
         if size < 0:
             raise ValueError("malformed result request")

@@ -137,8 +137,46 @@ def qcl_gradient_case(n, layers, theta_seed, target_seed):
             "gradient": list(rep.gradient), "losses": losses}
 
 
+def counts_cases():
+    """Counts mode (backend.py:234-251, 314-321): sampled tallies from the
+    reference for random circuits (with and without X/Z terms), and the
+    counts-mode DDCL / MC-VQE gradients."""
+    out = {"circuits": []}
+    for seed, n, n_gates, shots in ((1, 2, 6, 500), (2, 5, 30, 1000), (3, 8, 60, 4096), (4, 11, 90, 8192),
+                                     (5, 14, 120, 2000)):
+        rng = np.random.Generator(np.random.PCG64(3000 + seed))
+        batch = []
+        for i in range(4):
+            c = oracles.random_circuit(rng, n, n_gates, name=f"s{seed}c{i}")
+            if i % 2:
+                c = c.with_observable(oracles.random_pauli_term(rng, n, letters="XZ"))
+            batch.append(c)
+        buf = ResultBuffer(n_qubits=n)
+        StatevectorBackend().execute(buf, batch, ExecutionConfig(mode="counts", shots=shots, seed=11 * seed,
+                                                                  first_global_index=seed))
+        out["circuits"].append({
+            "n": n, "shots": shots, "seed": 11 * seed, "first_global_index": seed,
+            "batch": [{"gates": gates_json(c), "observable": obs_json(c.observable), "name": c.name} for c in batch],
+            "counts": [ch.counts for ch in buf.children]})
+    theta = random_angles(ddcl_parameter_count(4, 1), 7)
+    spec = DdclSpec(4, 1, theta, random_target_distribution(4, 8), shots=2048)
+    rep = ddcl_gradient(spec, VqpuPoolConfig(mode="counts", shots=2048, base_seed=6))
+    out["ddcl"] = {"n": 4, "layers": 1, "theta_seed": 7, "target_seed": 8, "shots": 2048, "base_seed": 6,
+                   "gradient": list(rep.gradient)}
+    ham = aiem_hamiltonian(random_aiem_coefficients(3, 8))
+    mspec = McvqeAnsatzSpec(random_cis_amplitudes(3, 9), random_angles(mcvqe_parameter_count(3), 10))
+    mrep = mcvqe_gradient(ham, mspec, VqpuPoolConfig(mode="counts", shots=512, base_seed=1))
+    out["mcvqe"] = {"n": 3, "coeff_seed": 8, "cis_seed": 9, "theta_seed": 10, "shots": 512, "base_seed": 1,
+                    "gradient": list(mrep.gradient)}
+    return out
+
+
 def main():
+    if "--counts-only" in sys.argv:
+        (OUT / "golden_counts.json").write_text(json.dumps(counts_cases()))
+        return
     t0 = time.time()
+    (OUT / "golden_counts.json").write_text(json.dumps(counts_cases()))
     small = {"generator": "tests/golden/make_golden.py", "reference": str(REF),
              "random_circuits": random_circuits()}
     print(f"random circuits {time.time() - t0:.1f}s", flush=True)
