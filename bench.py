@@ -337,8 +337,9 @@ def main():
         def step():
             return qv.mcvqe_gradient(ham, mspec, pool, backend_factory=_Factory(device, precision))
 
-    # vQPU b -> rank b mod world; 8 blocks per GPU keep the prefix-sharing
-    # work balanced across ranks (each rank runs its blocks as one batch)
+    # 8 vQPU blocks per GPU, dealt to ranks in zigzag order (vqpu.rank_of_block)
+    # so every rank gets parameters from every depth; each rank runs its blocks
+    # as one batch sharing one trunk
     pool = qv.VqpuPoolConfig(n_virtual_qpus=1 if world == 1 else 8 * world)
     engine = native.engine(device, precision)
 

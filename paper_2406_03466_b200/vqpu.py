@@ -146,6 +146,16 @@ def _dist_context():
     return None
 
 
+def rank_of_block(b: int, world: int) -> int:
+    """Zigzag (boustrophedon) block -> rank map: 0,1,..,W-1,W-1,..,1,0,...
+    Consecutive blocks of a shifted batch get steadily cheaper (later
+    parameters branch off the shared trunk later), so plain round-robin would
+    hand rank 0 the most expensive block of every round; zigzag cancels that
+    gradient to first order."""
+    r = b % (2 * world)
+    return r if r < world else 2 * world - 1 - r
+
+
 def execute_values(circuits: Sequence[Circuit], n_qubits: int, config: VqpuPoolConfig,
                    backend_factory: Callable[[], Accelerator], evaluate: Callable,
                    ) -> tuple[float, np.ndarray]:
@@ -154,9 +164,9 @@ def execute_values(circuits: Sequence[Circuit], n_qubits: int, config: VqpuPoolC
 
     Single process: one thread and backend per non-empty block (as
     `execute_parallel`).  Under torch.distributed with world size W > 1: block
-    b belongs to rank b mod W; each rank runs all of its blocks as one batch
-    on its GPU, then one NCCL all-gather (gloo on CPU) shares the values.
-    Values are a function of each circuit alone, so every split gives
+    b belongs to rank `rank_of_block(b, W)`; each rank runs all of its blocks
+    as one batch on its GPU, then one NCCL all-gather (gloo on CPU) shares the
+    values.  Values are a function of each circuit alone, so every split gives
     bitwise-identical results.
     """
     _validate_batch(circuits, n_qubits)
@@ -175,13 +185,14 @@ def execute_values(circuits: Sequence[Circuit], n_qubits: int, config: VqpuPoolC
 
     import torch
     rank, world = dist.get_rank(), dist.get_world_size()
-    mine = [b for i, b in enumerate(blocks) if i % world == rank]
+    owner = [rank_of_block(i, world) for i in range(len(blocks))]
+    mine = [b for i, b in enumerate(blocks) if owner[i] == rank]
     index = np.concatenate([np.arange(b.start, b.end) for b in mine]) if mine else np.zeros(0, np.int64)
     local = np.zeros(0, np.float64)
     if mine:
         backend = backend_factory()
         local = np.asarray(evaluate(backend, [circuits[i] for i in index]), dtype=np.float64)
-    per_rank = [sum(b.size for i, b in enumerate(blocks) if i % world == r) for r in range(world)]
+    per_rank = [sum(b.size for i, b in enumerate(blocks) if owner[i] == r) for r in range(world)]
     width = max(per_rank)
     use_cuda = dist.get_backend() == "nccl"
     device = torch.device("cuda", torch.cuda.current_device()) if use_cuda else torch.device("cpu")
@@ -193,7 +204,7 @@ def execute_values(circuits: Sequence[Circuit], n_qubits: int, config: VqpuPoolC
     gathered = recv.cpu().numpy().reshape(world, width)
     values = np.empty(len(circuits), np.float64)
     for r in range(world):
-        owned = [b for i, b in enumerate(blocks) if i % world == r]
+        owned = [b for i, b in enumerate(blocks) if owner[i] == r]
         cursor = 0
         for b in owned:
             values[b.start:b.end] = gathered[r, cursor:cursor + b.size]

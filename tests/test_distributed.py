@@ -47,6 +47,11 @@ def _worker(rank, world, port, n_circuits, n_vqpus, out):
         dist.destroy_process_group()
 
 
+def test_zigzag_block_owner():
+    assert [qv.vqpu.rank_of_block(b, 4) for b in range(10)] == [0, 1, 2, 3, 3, 2, 1, 0, 0, 1]
+    assert [qv.vqpu.rank_of_block(b, 1) for b in range(3)] == [0, 0, 0]
+
+
 @pytest.mark.parametrize("n_circuits,n_vqpus", [(10, 4), (7, 16), (2688, 16), (5, 1)])
 def test_execute_values_two_ranks(n_circuits, n_vqpus):
     manager = mp.Manager()
@@ -57,5 +62,6 @@ def test_execute_values_two_ranks(n_circuits, n_vqpus):
     for rank in range(2):
         values, seen = out[rank]
         assert values == want
-        mine = [f"c{i}" for j, b in enumerate(blocks) if j % 2 == rank for i in range(b.start, b.end)]
+        mine = [f"c{i}" for j, b in enumerate(blocks) if qv.vqpu.rank_of_block(j, 2) == rank
+                for i in range(b.start, b.end)]
         assert seen == mine
