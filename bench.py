@@ -417,14 +417,16 @@ def main():
                 "circuits_per_step": circuits, "step": "one full parameter-shift gradient",
                 "full_gradient_s": e2e_ms_max / steps / 1e3,
                 "full_gradient_device_s": dev_ms_max / steps / 1e3,
-                "parallelism": f"vqpu{pool.n_virtual_qpus}->gpu{world} (round-robin), NCCL all-gather of losses",
+                "parallelism": f"vqpu{pool.n_virtual_qpus}->gpu{world} (zigzag blocks), NCCL all-gather of losses",
+                "shift_mode": "pair (psi+- = (Psi0 -+ i Xi_k)/sqrt2: one extra state per parameter)"
+                if kind == "qcl" and n > 12 else "direct",
                 "passes_per_circuit": passes, "tile_bits": tile,
                 "hbm_sweeps_per_step": float(sm[6]) / steps, "hbm_sweeps_without_prefix_sharing": float(sm[7]) / steps,
                 "l2": "states (2^n x 16 B) far exceed the 126 MB L2; no flush needed",
                 "gradient_checksum": float(np.sum(grad)), "seed": s,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                         "frac": achieved / hbm_peak if hbm_peak else None, **_ncu_traffic(),
                          "kernel": "pass_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                          "fp64_achieved_tflops": fp_rate, "fp64_peak_tflops": fp64_peak,
                          "fp64_peak_source": "cuBLAS DGEMM 8192^3 measured in this run" if fp64_peak else None},
@@ -453,6 +455,19 @@ class _Factory:
     def __call__(self):
         import paper_2406_03466_b200 as qv
         return qv.B200Backend(device=self.device, precision=self.precision)
+
+
+def _ncu_traffic():
+    """DRAM bytes of one pass_kernel launch from the committed ncu --set full
+    capture (profiles/ncu_pass_kernel.json), beside that launch's algorithmic
+    bytes; null if the capture is absent."""
+    try:
+        prof = json.loads((ROOT / "profiles" / "ncu_pass_kernel.json").read_text())
+        launch = prof["launches"][0]
+        return {"traffic": launch["traffic_bytes"], "traffic_algorithmic_bytes": launch["algorithmic_bytes"],
+                "traffic_launch": launch["what"], "traffic_source": "profiles/ncu_pass_kernel.json"}
+    except Exception:
+        return {"traffic": None}
 
 
 def _measured_peaks():
