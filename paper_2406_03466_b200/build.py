@@ -65,6 +65,17 @@ def build_trace(force: bool = False) -> Path:
     return TRACE
 
 
+def build_variant(name: str, defines: list[str], force: bool = False) -> Path:
+    """Experimental build with extra -D tuning macros (QV_C128_TILE_BITS, ...),
+    selected at run time with QVB200_LIB=<path>.  Used by A/B measurements."""
+    target = PKG / f"libqvb200_{name}.so"
+    if force or _stale(target, PRODUCT_DEPS):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+              *[f"-D{d}" for d in defines], "-cudart", "static", f"-I{INCLUDE}", f"-I{CSRC}", "-o", target,
+              *PRODUCT_SOURCES])
+    return target
+
+
 def build_plancheck(force: bool = False) -> Path:
     if force or _stale(PLANCHECK, PLANCHECK_DEPS):
         _run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", f"-I{CSRC}", "-o", PLANCHECK, *PLANCHECK_SOURCES])

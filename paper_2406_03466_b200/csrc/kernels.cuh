@@ -150,11 +150,20 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // DB (double buffer): two tile buffers; the next item's tile streams in with
 // cp.async while the current one is computed and written back, so HBM, the
 // shared-memory pipe and the FP64 pipe work concurrently inside one CTA.
-template <typename T, int TB, bool DB>
+//
+// MODE 0: single-tile launches (every epilogue, incl. the whole-state F_SINGLE
+// ones).  MODE 1 / 2: multi-tile launches -- 1 stores (F_STORE, F_NORM,
+// F_SUPPORT) and defers the global stores behind the next tile's load issue,
+// 2 is the shift-pair epilogue (F_PAIR).  Separate instantiations keep each
+// variant's register footprint to what it uses.
+template <typename T, int TB, bool DB, int MODE>
 __global__ void __launch_bounds__(pass_threads(TB), (DB || TB >= 9 ? 1 : TB == 8 ? 2 : 4))
 pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent,
             int nstates, int unused, EpiArgs ep) {
     typedef typename Cx<T>::V V;
+    constexpr bool MT = MODE != 0;
+    constexpr bool PAIR = MODE != 1;
+    constexpr bool PLAIN = MODE != 2;
     constexpr int NT = 1 << TB;             // active threads (TB < 5: a partial warp)
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);   // register bits per group
     constexpr int NA = 1 << R;                           // amplitudes per thread
@@ -188,14 +197,17 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
             if ((x >> j) & 1) o |= 1ull << pd.obits[j];
         return o;
     };
-    auto issue_load = [&](int64_t w, unsigned char* dst) {   // NA async 8/16-byte copies per thread
+    auto load_src = [&](int64_t w) -> const V* {   // this thread's first source amplitude of item w
         const V* in = reinterpret_cast<const V*>(ent[w % nstates].in);
-        if (in == nullptr || !active) return;
-        const V* src = in + (outer_of(w / nstates) | tg);
+        return (in == nullptr || !active) ? nullptr : in + (outer_of(w / nstates) | tg);
+    };
+    auto issue_from = [&](const V* src, unsigned char* dst) {   // NA async 8/16-byte copies per thread
+        if (src == nullptr) return;
 #pragma unroll
         for (int it = 0; it < NA; ++it)
             cp_async<sizeof(V)>(dst + (size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V), src + pd.g_hi[it]);
     };
+    auto issue_load = [&](int64_t w, unsigned char* dst) { issue_from(load_src(w), dst); };
     if (blockIdx.x < items) issue_load(blockIdx.x, smem_raw);
     cp_async_commit();
 
@@ -230,11 +242,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
                 }
             }
         }
-        if (!DB && i > 0) {
-            issue_load(w, tileb);
-            cp_async_commit();
-        }
-        cp_async_wait<0>();   // this item's tile has landed
+        cp_async_wait<0>();   // this item's tile has landed (issued by the previous item)
         __syncthreads();
         QV_MARK(1);
         if (DB && w + G < items) {   // stream the next item's tile in behind this one's math
@@ -296,8 +304,23 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
             }
         }
         // ---- store / reduce ----------------------------------------------------
+        // Every shared-memory read of this tile (the thread's own amplitudes
+        // into `vals`, support / Pauli / pair epilogues) happens before the
+        // closing barrier; the next item's load is then issued before this
+        // item's global stores, so its latency overlaps the store phase.
         double acc = 0.0;
-        if (ep.flags & F_PAIR) {
+        V vals[NA];
+        // the next item's source address, computed while few registers are live
+        const V* next_src = (!DB && w + G < items) ? load_src(w + G) : nullptr;
+        if (ep.flags & F_SUPPORT) {
+            const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
+            double* row = ep.sup_out + e.rslot * (ep.S + 1);
+            for (int32_t i = lo + tid; i < hi; i += blockDim.x) {
+                const uint32_t slot = apply_cols(pd.fin, K, (uint32_t)ep.sup_local[i]);
+                row[ep.sup_pos[i]] = norm2(*reinterpret_cast<const V*>(tileb + (size_t)slot * sizeof(V)));
+            }
+        }
+        if (PAIR && (ep.flags & F_PAIR)) {
             // shift pair: this tile holds Xi, `aux` the unshifted output Psi0.
             // Per tile: sum |Psi0|^2, sum |Xi|^2, sum Im(Psi0 conj(Xi)); per
             // support index the same three terms (finalize_pair_kernel forms
@@ -337,29 +360,26 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
                 row[1] = norm2(v);
                 row[2] = (double)u.y * (double)v.x - (double)u.x * (double)v.y;
             }
-        } else if (active) {
-            V* __restrict__ dst = out + (outer | tg);
+        } else if (PLAIN && active) {
 #pragma unroll
             for (int it = 0; it < NA; ++it) {
-                const V v = *reinterpret_cast<const V*>(tileb + (size_t)(fslot ^ pd.fin_hi[it]) * sizeof(V));
-                if (store) __stcs(dst + pd.g_hi[it], v);
-                acc += norm2(v);
+                vals[it] = *reinterpret_cast<const V*>(tileb + (size_t)(fslot ^ pd.fin_hi[it]) * sizeof(V));
+                acc += norm2(vals[it]);
+            }
+            if constexpr (!MT) {
+                if (store) {
+                    V* __restrict__ dst = out + (outer | tg);
+#pragma unroll
+                    for (int it = 0; it < NA; ++it) __stcs(dst + pd.g_hi[it], vals[it]);
+                }
             }
         }
         QV_MARK(62);
-        if (ep.flags & F_NORM) {
+        if (!MT && (ep.flags & F_NORM)) {
             const double s = block_sum(acc, sred);
             if (tid == 0) ep.partial[e.pslot * ntiles + x] = s;
         }
-        if (ep.flags & F_SUPPORT) {
-            const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
-            double* row = ep.sup_out + e.rslot * (ep.S + 1);
-            for (int32_t i = lo + tid; i < hi; i += blockDim.x) {
-                const uint32_t slot = apply_cols(pd.fin, K, (uint32_t)ep.sup_local[i]);
-                row[ep.sup_pos[i]] = norm2(*reinterpret_cast<const V*>(tileb + (size_t)slot * sizeof(V)));
-            }
-        }
-        if (ep.flags & F_SINGLE) {
+        if (!MT && (ep.flags & F_SINGLE)) {
             // the tile is the whole state (ntiles == 1)
             const double total = block_sum(acc, sred);
             const int64_t dim = 1ll << ep.n;
@@ -419,7 +439,25 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
                 }
             }
         }
+        if (MT && PLAIN && store && active && !(ep.flags & F_PAIR)) {   // first half before the barrier
+            V* __restrict__ dst = out + (outer | tg);
+#pragma unroll
+            for (int it = 0; it < NA / 2; ++it) __stcs(dst + pd.g_hi[it], vals[it]);
+        }
         __syncthreads();   // the next tile overwrites the shared tile
+        if (!DB) {
+            issue_from(next_src, smem_raw);
+            cp_async_commit();
+        }
+        if (MT && PLAIN && store && active && !(ep.flags & F_PAIR)) {
+            V* __restrict__ dst = out + (outer | tg);
+#pragma unroll
+            for (int it = NA / 2; it < NA; ++it) __stcs(dst + pd.g_hi[it], vals[it]);
+        }
+        if (MT && (ep.flags & F_NORM)) {   // sred is outside the tile: safe beside the next load
+            const double s = block_sum(acc, sred);
+            if (tid == 0) ep.partial[e.pslot * ntiles + x] = s;
+        }
     }
 }
 
@@ -427,12 +465,14 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
 // slots[2*b] = result slot, slots[2*b+1] = partial slot.
 __global__ void finalize_dist_kernel(const int64_t* __restrict__ slots, int64_t ntiles, const double* __restrict__ partial,
                                      double* __restrict__ sup_out, int64_t S, const double* __restrict__ target,
-                                     double* __restrict__ js_out, int want_js) {
+                                     double* __restrict__ js_out, int want_js, int unit_norm) {
     __shared__ double sred[32];
     const int64_t r = slots[2 * blockIdx.x], ps = slots[2 * blockIdx.x + 1];
     double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) acc += partial[ps * ntiles + i];
-    const double total = block_sum(acc, sred);
+    if (!unit_norm)
+        for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) acc += partial[ps * ntiles + i];
+    // light-cone runs do not sweep the norm: a unitary circuit keeps it at 1
+    const double total = unit_norm ? 1.0 : block_sum(acc, sred);
     double* row = sup_out + r * (S + 1);
     double jsum = 0.0, qsum = 0.0;
     for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
@@ -455,7 +495,7 @@ __global__ void finalize_dist_kernel(const int64_t* __restrict__ slots, int64_t 
 // slots[2*b] = result slot, slots[2*b+1] = partial slot; out[2r], out[2r+1].
 __global__ void finalize_pair_kernel(const int64_t* __restrict__ slots, int64_t ntiles, const double* __restrict__ partial,
                                      const double* __restrict__ pair_sup, int64_t S, const double* __restrict__ target,
-                                     double* __restrict__ out) {
+                                     double* __restrict__ out, int unit_norm) {
     __shared__ double sred[32];
     const int64_t r = slots[2 * blockIdx.x], ps = slots[2 * blockIdx.x + 1];
     double a = 0.0, b = 0.0, c = 0.0;
@@ -465,7 +505,12 @@ __global__ void finalize_pair_kernel(const int64_t* __restrict__ slots, int64_t 
         b += p[1];
         c += p[2];
     }
-    const double A = block_sum(a, sred), B = block_sum(b, sred), C = block_sum(c, sred);
+    double A = block_sum(a, sred), B = block_sum(b, sred), C = block_sum(c, sred);
+    if (unit_norm) {   // light-cone run: |Psi0| = |Xi| = 1 and Im<Psi0|Xi> = 0 exactly
+        A = 1.0;
+        B = 1.0;
+        C = 0.0;
+    }
     const double tp = A + B - 2.0 * C, tm = A + B + 2.0 * C;
     double jp = 0.0, jm = 0.0, sp = 0.0, sm = 0.0;
     for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {

@@ -33,10 +33,13 @@ __host__ __device__
 #endif
 constexpr int reg_bits(int precision) { return precision == 0 ? QV_C128_REG_BITS : 4; }
 // widest tile (multi-tile registers): 2^12 complex128 / 2^13 complex64 = 64 KiB
+#ifndef QV_C128_TILE_BITS
+#define QV_C128_TILE_BITS 12
+#endif
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-constexpr int max_tile_bits(int precision) { return precision == 0 ? 12 : 13; }
+constexpr int max_tile_bits(int precision) { return precision == 0 ? QV_C128_TILE_BITS : 13; }
 constexpr int kMaxTileBits = 13;     // 2^13 amplitudes (64 KiB at complex64, 128 KiB c128)
 constexpr int kMaxQubits = 40;
 

@@ -136,4 +136,21 @@ int qvp_plan_stats(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* 
     }
 }
 
+// Tile bit set of every pass as a bit mask (global index bits).
+int qvp_plan_pass_masks(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                        int precision, int max_tile_bits, uint64_t* masks, int32_t cap) {
+    try {
+        const Topology topo = make_topo(n, n_gates, kinds, q0, q1);
+        const Plan plan = build_plan(topo, precision, max_tile_bits);
+        for (size_t p = 0; p < plan.passes.size() && (int32_t)p < cap; ++p) {
+            uint64_t m = 0;
+            for (int b : plan.passes[p].S) m |= 1ull << b;
+            masks[p] = m;
+        }
+        return (int)plan.passes.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 }  // extern "C"

@@ -78,8 +78,6 @@ struct CachedPlan {
     DevBuf<GroupDesc> d_groups;
 };
 
-constexpr int kNT128 = 256;   // threads per CTA at k = 12, complex128
-constexpr int kNT64 = 512;    // threads per CTA at k = 13, complex64
 
 uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
     const unsigned char* p = static_cast<const unsigned char*>(data);
@@ -265,7 +263,7 @@ using PassFn = void (*)(const PassDesc, const GroupDesc*, const LaunchEntry*, in
 
 template <typename T, int... TBs>
 constexpr std::array<PassFn<T>, sizeof...(TBs)> pass_table(std::integer_sequence<int, TBs...>) {
-    return {{&pass_kernel<T, TBs, false>...}};
+    return {{&pass_kernel<T, TBs, false, 0>...}};
 }
 // TB = tile bits - 4: 0..8 for complex128 (k <= 12), 0..9 for complex64 (k <= 13)
 template <typename T>
@@ -278,16 +276,31 @@ template <typename T>
 constexpr int multi_tile_tb() {
     return max_tile_bits(sizeof(T) == 8 ? 0 : 1) - reg_bits(sizeof(T) == 8 ? 0 : 1);
 }
+// Double buffering (next tile streaming in behind the current one's math)
+// needs two widest tiles in shared memory and so leaves room for only one CTA
+// per SM.  Off by default: measured on B200 (28q x 8L gradient), two
+// independent single-buffered CTAs per SM -- one loading or storing while the
+// other computes -- are 13% faster (52.7 s vs 60.5 s).
+#ifndef QV_DOUBLE_BUFFER
+#define QV_DOUBLE_BUFFER 0
+#endif
 template <typename T>
-PassFn<T> pass_kernel_db() {
-    return &pass_kernel<T, multi_tile_tb<T>(), true>;
+constexpr bool multi_tile_db() {
+    return QV_DOUBLE_BUFFER && (sizeof(typename Cx<T>::V) << max_tile_bits(sizeof(T) == 8 ? 0 : 1)) <= 96 * 1024;
+}
+// multi-tile launches (widest tile): deferred stores, optional double buffer
+template <typename T>
+PassFn<T> pass_kernel_multi(bool pair) {
+    return pair ? &pass_kernel<T, multi_tile_tb<T>(), multi_tile_db<T>(), 2>
+                : &pass_kernel<T, multi_tile_tb<T>(), multi_tile_db<T>(), 1>;
 }
 
 template <typename T>
 void set_kernel_attributes() {
     for (auto fn : pass_kernels<T>())
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(pass_kernel_db<T>(), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (bool pair : {false, true})
+        CK(cudaFuncSetAttribute(pass_kernel_multi<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 
 template <typename T>
@@ -295,11 +308,12 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
                  int64_t ntiles, const EpiArgs& ep, bool generated) {
     typedef typename Cx<T>::V V;
     const int tb = pd.k - reg_bits(sizeof(T) == 8 ? 0 : 1);
-    const bool db = ntiles > 1 && tb == multi_tile_tb<T>();
+    const bool multi = ntiles > 1 && tb == multi_tile_tb<T>();
+    const bool db = multi && multi_tile_db<T>();
     const size_t smem = (sizeof(V) << pd.k) * (db ? 2 : 1) + (size_t)pd.ng * sizeof(GroupDesc) +
                         (size_t)pd.nm * 4 * sizeof(V) + 32 * sizeof(double);
     const int threads = pass_threads(tb);
-    PassFn<T> fn = db ? pass_kernel_db<T>() : pass_kernels<T>()[tb];
+    PassFn<T> fn = multi ? pass_kernel_multi<T>((ep.flags & F_PAIR) != 0) : pass_kernels<T>()[tb];
     // persistent CTAs: enough per state to fill every SM at full occupancy
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
@@ -347,8 +361,38 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     E.stats[0] += 1;
     // algorithmic FP64/FP32 work: 2^(n-1) pairs x 28 flops per fused 2x2
     // matrix (a |0> input only computes tile 0 of a multi-tile state)
-    const double amps = (generated && ntiles > 1) ? (double)(1ll << pd.k) : std::ldexp(1.0, ep.n);
+    const double amps = generated ? (double)(1ll << pd.k) : (double)ntiles * (double)(1ll << pd.k);
     E.stats[11] += (double)nstates * amps * 14.0 * pd.nm;
+}
+
+// Backward light cone of a support-restricted output (SUPPORT / JS results).
+// A bit that is zero in every support index and that no pass from p on
+// touches is a spectator: the final amplitudes on the support only depend on
+// the inputs of pass p whose spectator bits are zero.  cone[p] = the bits
+// pass p must range over (support bits | tile bits of passes p..P-1); pass p
+// then runs on 2^|outer bits in cone[p]| tiles instead of all of them.  For the
+// QCL benchmarks (support = the 2^10 low indices) the last passes of every
+// circuit touch 1, 4, 1024 tiles instead of 2^16.
+std::vector<uint64_t> support_cone(const Plan& plan, const uint64_t* support, int64_t S) {
+    uint64_t acc = 0;
+    for (int64_t s = 0; s < S; ++s) acc |= support[s];
+    std::vector<uint64_t> cone(plan.passes.size());
+    for (size_t p = plan.passes.size(); p-- > 0;) {
+        for (int b : plan.passes[p].S) acc |= 1ull << b;
+        cone[p] = acc;
+    }
+    return cone;
+}
+
+// The pass restricted to the tiles whose outer bits outside `cone` are zero.
+PassDesc restrict_pass(const PassDesc& pd, uint64_t cone) {
+    PassDesc r = pd;
+    int m = 0;
+    for (int j = 0; j < pd.n_outer; ++j)
+        if ((cone >> pd.obits[j]) & 1) r.obits[m++] = pd.obits[j];
+    for (int j = m; j < (int)sizeof(r.obits); ++j) r.obits[j] = 0;
+    r.n_outer = m;
+    return r;
 }
 
 // Support indices bucketed by the tile of the last pass that holds them
@@ -509,10 +553,22 @@ void GroupRun::run() {
     } else {
         const int k = plan.k;
         const int64_t ntiles = 1ll << (n - k);
-        ep.ntiles = ntiles;
         (void)k;
-        if (ep.S > 0) upload_support_csr(E, plan.pdesc[P - 1], R->support, ep);
         const bool dist = R->kind == QV_OUT_SUPPORT || R->kind == QV_OUT_JS;
+        // support-restricted outputs run every pass on its light cone only;
+        // the state norm is then not swept (unitary circuits keep it at 1)
+        std::vector<PassDesc> rpd(plan.pdesc.begin(), plan.pdesc.end());
+        std::vector<int64_t> rtiles(P, ntiles);
+        if (dist) {
+            const std::vector<uint64_t> cone = support_cone(plan, R->support, ep.S);
+            for (int p = 0; p < P; ++p) {
+                rpd[p] = restrict_pass(plan.pdesc[p], cone[p]);
+                rtiles[p] = 1ll << rpd[p].n_outer;
+            }
+        }
+        const bool unit_norm = rtiles[P - 1] < ntiles;
+        ep.ntiles = rtiles[P - 1];
+        if (ep.S > 0) upload_support_csr(E, rpd[P - 1], R->support, ep);
         const bool need_state_out = !dist;   // Pauli / full read the stored state
 
         // pass signatures per unique state
@@ -569,10 +625,11 @@ void GroupRun::run() {
                         ents.push_back({in, o, d_mats + (size_t)u * slots8, u, b, 0});
                     }
                     int flags = F_STORE;
-                    if (lastp && dist) flags = F_NORM | F_SUPPORT;
+                    if (lastp && dist) flags = unit_norm ? F_SUPPORT : F_NORM | F_SUPPORT;
                     if (lastp && probs) flags = F_STORE | F_NORM;
                     const double rd = (pp == p && p == 0) ? 0.0 : 1.0, wr = (flags & F_STORE) ? 1.0 : 0.0;
-                    sched.push_back({L_PASS, pp, off, nb, flags, nullptr, 0, 0, nb * (double)state_bytes * (rd + wr)});
+                    const double frac = (double)rtiles[pp] / (double)ntiles;
+                    sched.push_back({L_PASS, pp, off, nb, flags, nullptr, 0, 0, nb * (double)state_bytes * frac * (rd + wr)});
                 }
                 if (dist || probs) {
                     const size_t off = slots_tab.size();
@@ -620,7 +677,8 @@ void GroupRun::run() {
             alive.swap(stay);
             const size_t off = ents.size();
             ents.push_back({p == 0 ? nullptr : (const void*)trunk, (void*)trunk, d_mats + (size_t)alive[0] * slots8, alive[0], 0, 0});
-            sched.push_back({L_PASS, p, off, 1, F_STORE, nullptr, 0, 0, (double)state_bytes * ((p == 0 ? 0 : 1) + 1)});
+            sched.push_back({L_PASS, p, off, 1, F_STORE, nullptr, 0, 0,
+                             (double)state_bytes * (double)rtiles[p] / (double)ntiles * ((p == 0 ? 0 : 1) + 1)});
         }
         if (!alive.empty()) throw std::runtime_error("scheduler left states unfinished");
 
@@ -636,12 +694,13 @@ void GroupRun::run() {
                 e2.flags = l.flags;
                 e2.partial = partial;
                 if (!(l.flags & F_SUPPORT)) e2.sup_off = nullptr;
-                launch_pass<T>(E, plan.pdesc[l.pass], cp.d_groups.p, dent + l.off, l.count, ntiles, e2, l.pass == 0);
+                launch_pass<T>(E, rpd[l.pass], cp.d_groups.p, dent + l.off, l.count, rtiles[l.pass], e2, l.pass == 0);
                 E.stats[1] += l.count;
                 E.stats[4] += l.bytes;
             } else if (l.kind == L_FINAL_DIST) {
-                finalize_dist_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, ntiles, partial, ep.sup_out, ep.S,
-                                                                     ep.target, ep.js_out, R->kind == QV_OUT_JS);
+                finalize_dist_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, rtiles[P - 1], partial, ep.sup_out,
+                                                                     ep.S, ep.target, ep.js_out, R->kind == QV_OUT_JS,
+                                                                     unit_norm);
                 CK(cudaGetLastError());
                 E.stats[0] += 1;
             } else if (l.kind == L_FULL) {
@@ -860,17 +919,30 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     std::memset(&ep, 0, sizeof(ep));
     ep.n = n;
     ep.S = R->support_count;
-    ep.ntiles = 1ll << (n - plan.k);
-    const int64_t ntiles = ep.ntiles;
+    const int64_t ntiles = 1ll << (n - plan.k);
+    // every pass on the support's light cone (see support_cone); the norms
+    // of Psi0 and Xi are then 1 and Im<Psi0|Xi> = 0 exactly (psi+- = (Psi0 -+
+    // i Xi)/sqrt2 are both unit vectors), instead of being swept
+    std::vector<PassDesc> rpd(P);
+    std::vector<int64_t> rtiles(P);
+    {
+        const std::vector<uint64_t> cone = support_cone(plan, R->support, ep.S);
+        for (int p = 0; p < P; ++p) {
+            rpd[p] = restrict_pass(plan.pdesc[p], cone[p]);
+            rtiles[p] = 1ll << rpd[p].n_outer;
+        }
+    }
+    const bool unit_norm = rtiles[P - 1] < ntiles;
+    ep.ntiles = rtiles[P - 1];
     uint64_t* dsu = E.d_support.get(std::max<int64_t>(1, ep.S));
     double* dta = E.d_target.get(std::max<int64_t>(1, ep.S));
     if (ep.S > 0) {
         h2d(E, dsu, R->support, ep.S * 8);
         h2d(E, dta, R->target, ep.S * 8);
-        upload_support_csr(E, plan.pdesc[P - 1], R->support, ep);
+        upload_support_csr(E, rpd[P - 1], R->support, ep);
     } else {
-        std::vector<int32_t> zeros(ntiles + 1, 0);
-        int32_t* doff = E.d_sup_off.get(ntiles + 1);
+        std::vector<int32_t> zeros(ep.ntiles + 1, 0);
+        int32_t* doff = E.d_sup_off.get(ep.ntiles + 1);
         h2d(E, doff, zeros.data(), zeros.size() * 4);
         ep.sup_off = doff;
     }
@@ -892,12 +964,13 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
 
     // ---- schedule ----------------------------------------------------------
     struct L { bool pass; int p; size_t off; int count; int flags; double bytes; };
+    auto frac = [&](int p) { return (double)state_bytes * (double)rtiles[p] / (double)ntiles; };   // bytes per sweep
     std::vector<L> sched;
     std::vector<LaunchEntry> ents;
     std::vector<int64_t> slots_tab;
     for (int p = 0; p < P; ++p) {   // phase 1: Psi0
         ents.push_back({p == 0 ? nullptr : (const void*)psi0, (void*)psi0, mats_of(0), 0, 0, nullptr});
-        sched.push_back({true, p, ents.size() - 1, 1, F_STORE, (double)state_bytes * ((p ? 1 : 0) + 1)});
+        sched.push_back({true, p, ents.size() - 1, 1, F_STORE, frac(p) * ((p ? 1 : 0) + 1)});
     }
     std::vector<std::vector<int64_t>> by_pass(P);
     for (int64_t j = 0; j < nshift; ++j) by_pass[start_pass[j]].push_back(j);
@@ -917,8 +990,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
                                     (const void*)psi0});
                 }
                 const double rd = (pp == p && p == 0) ? 0.0 : 1.0;
-                sched.push_back({true, pp, off, nb, lastp ? F_PAIR : F_STORE,
-                                 nb * (double)state_bytes * (lastp ? 2.0 : rd + 1.0)});
+                sched.push_back({true, pp, off, nb, lastp ? F_PAIR : F_STORE, nb * frac(pp) * (lastp ? 2.0 : rd + 1.0)});
             }
             const size_t off = slots_tab.size();
             for (int b = 0; b < nb; ++b) { slots_tab.push_back(D[b0 + b]); slots_tab.push_back(b); }
@@ -926,7 +998,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
         }
         if (p < last_needed) {   // advance the trunk by pass p
             ents.push_back({p == 0 ? nullptr : (const void*)trunk, (void*)trunk, mats_of(0), 0, 0, nullptr});
-            sched.push_back({true, p, ents.size() - 1, 1, F_STORE, (double)state_bytes * ((p ? 1 : 0) + 1)});
+            sched.push_back({true, p, ents.size() - 1, 1, F_STORE, frac(p) * ((p ? 1 : 0) + 1)});
         }
     }
     LaunchEntry* dent = E.d_entries.get(ents.size());
@@ -940,12 +1012,12 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
             EpiArgs e2 = ep;
             e2.flags = l.flags;
             e2.partial = partial;
-            launch_pass<T>(E, plan.pdesc[l.p], cp.d_groups.p, dent + l.off, l.count, ntiles, e2, l.p == 0);
+            launch_pass<T>(E, rpd[l.p], cp.d_groups.p, dent + l.off, l.count, rtiles[l.p], e2, l.p == 0);
             E.stats[1] += l.count;
             E.stats[4] += l.bytes;
         } else {
-            finalize_pair_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, ntiles, partial, ep.pair_sup, ep.S,
-                                                                 ep.target, d_out);
+            finalize_pair_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, rtiles[P - 1], partial, ep.pair_sup,
+                                                                 ep.S, ep.target, d_out, unit_norm);
             CK(cudaGetLastError());
             E.stats[0] += 1;
         }

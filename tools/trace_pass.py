@@ -19,7 +19,8 @@ ROOT = Path(__file__).resolve().parent.parent
 def main():
     args = sys.argv[1:] or ["26", "2", "2"]
     out = "/tmp/qv_trace.bin"
-    env = dict(os.environ, QVB200_LIB=str(ROOT / "paper_2406_03466_b200" / "libqvb200_trace.so"),
+    lib = os.environ.get("QVB200_TRACE_LIB") or str(ROOT / "paper_2406_03466_b200" / "libqvb200_trace.so")
+    env = dict(os.environ, QVB200_LIB=lib,
                QVB200_TRACE_OUT=out)
     subprocess.run([sys.executable, str(ROOT / "tools" / "profile_pass.py"), *args], env=env, check=True)
     raw = Path(out).read_bytes()
