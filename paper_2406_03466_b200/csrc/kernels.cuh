@@ -157,7 +157,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // 2 is the shift-pair epilogue (F_PAIR).  Separate instantiations keep each
 // variant's register footprint to what it uses.
 template <typename T, int TB, bool DB, int MODE>
-__global__ void __launch_bounds__(pass_threads(TB), (DB || TB >= 9 ? 1 : TB == 8 ? 2 : 4))
+#ifndef QV_TB9_MIN_BLOCKS
+#define QV_TB9_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(pass_threads(TB), (DB ? 1 : TB >= 9 ? QV_TB9_MIN_BLOCKS : TB == 8 ? 2 : 4))
 pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent,
             int nstates, int unused, EpiArgs ep) {
     typedef typename Cx<T>::V V;
@@ -173,6 +176,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
     GroupDesc* sg = reinterpret_cast<GroupDesc*>(smem_raw + TILE * (DB ? 2 : 1));
     V* smat = reinterpret_cast<V*>(sg + pd.ng);                            // 4 complex per matrix
     double* sred = reinterpret_cast<double*>(smat + (size_t)pd.nm * 4);
+    uint64_t* otab = reinterpret_cast<uint64_t*>(sred + 32);   // MT: 4 x 256 outer-offset tables
     (void)unused;
 
     const int tid = threadIdx.x;
@@ -184,6 +188,16 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         uint4* gdst = reinterpret_cast<uint4*>(sg);
         for (int i = tid; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
     }
+    if constexpr (MT) {   // outer offset of tile x = OR of 4 byte-indexed tables (n - k <= 32)
+        for (int idx = tid; idx < 1024; idx += blockDim.x) {
+            const int b = idx >> 8, v = idx & 255;
+            uint64_t o = 0;
+            for (int j = 0; j < 8; ++j)
+                if (((v >> j) & 1) && 8 * b + j < pd.n_outer) o |= 1ull << pd.obits[8 * b + j];
+            otab[idx] = o;
+        }
+        __syncthreads();
+    }
     const bool active = tid < NT;
     // per-thread parts of the load / store maps (tile-independent)
     uint32_t tslot = 0, fslot = 0;
@@ -191,16 +205,25 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
 #pragma unroll
     for (int j = 0; j < TB; ++j)
         if ((tid >> j) & 1) { tslot ^= pd.swz[j]; fslot ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
-    auto outer_of = [&](int64_t x) {
-        uint64_t o = 0;
-        for (int j = 0; j < pd.n_outer; ++j)
-            if ((x >> j) & 1) o |= 1ull << pd.obits[j];
-        return o;
+    auto outer_of = [&](int64_t x) -> uint64_t {
+        if constexpr (MT) {
+            return otab[x & 255] | otab[256 + ((x >> 8) & 255)] | otab[512 + ((x >> 16) & 255)] |
+                   otab[768 + ((x >> 24) & 255)];
+        } else {
+            uint64_t o = 0;
+            for (int j = 0; j < pd.n_outer; ++j)
+                if ((x >> j) & 1) o |= 1ull << pd.obits[j];
+            return o;
+        }
     };
-    auto load_src = [&](int64_t w) -> const V* {   // this thread's first source amplitude of item w
-        const V* in = reinterpret_cast<const V*>(ent[w % nstates].in);
-        return (in == nullptr || !active) ? nullptr : in + (outer_of(w / nstates) | tg);
+    // item w = x * nstates + y (state fastest); CTA items advance by G = gx * nstates + gy
+    const int64_t gx = G / nstates;
+    const int gy = (int)(G % nstates);
+    auto src_of = [&](int64_t xx, int yy) -> const V* {   // this thread's first source amplitude of an item
+        const V* in = reinterpret_cast<const V*>(ent[yy].in);
+        return (in == nullptr || !active) ? nullptr : in + (outer_of(xx) | tg);
     };
+    auto load_src = [&](int64_t w) -> const V* { return src_of(w / nstates, (int)(w % nstates)); };
     auto issue_from = [&](const V* src, unsigned char* dst) {   // NA async 8/16-byte copies per thread
         if (src == nullptr) return;
 #pragma unroll
@@ -214,9 +237,12 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
     int cur_y = -1;
     LaunchEntry e;
     int64_t i = 0;
+    int64_t x = (int64_t)blockIdx.x / nstates;
+    int y = (int)((int64_t)blockIdx.x % nstates);
     for (int64_t w = blockIdx.x; w < items; w += G, ++i) {
-        const int y = (int)(w % nstates);
-        const int64_t x = w / nstates;
+        int64_t xn = x + gx;   // the next item's coordinates
+        int yn = y + gy;
+        if (yn >= nstates) { yn -= nstates; ++xn; }
         QV_MARK(0);
         if (y != cur_y) {   // stage this state's matrices (the previous item is finished)
             e = ent[y];
@@ -246,7 +272,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         __syncthreads();
         QV_MARK(1);
         if (DB && w + G < items) {   // stream the next item's tile in behind this one's math
-            issue_load(w + G, smem_raw + ((i & 1) ? 0 : TILE));
+            issue_from(src_of(xn, yn), smem_raw + ((i & 1) ? 0 : TILE));
             cp_async_commit();
         }
         // ---- register groups --------------------------------------------------
@@ -311,7 +337,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         double acc = 0.0;
         V vals[NA];
         // the next item's source address, computed while few registers are live
-        const V* next_src = (!DB && w + G < items) ? load_src(w + G) : nullptr;
+        const V* next_src = (!DB && w + G < items) ? src_of(xn, yn) : nullptr;
         if (ep.flags & F_SUPPORT) {
             const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
             double* row = ep.sup_out + e.rslot * (ep.S + 1);
@@ -458,7 +484,258 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
             const double s = block_sum(acc, sred);
             if (tid == 0) ep.partial[e.pslot * ntiles + x] = s;
         }
+        x = xn;
+        y = yn;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Ring pass kernel (multi-tile, complex128): one 512-thread CTA per SM made of
+// two 256-thread teams that share a ring of three tile buffers.  Item i of the
+// CTA (items c, c + G, c + 2G, ...) belongs to team i mod 2 and lives in buffer
+// i mod 3; the team that finishes item i issues the cp.async load of item i + 3
+// into the buffer it just drained, and an mbarrier per buffer (256 arrivals,
+// cp.async.mbarrier.arrive.noinc) tells the other team when it has landed.
+// Each team therefore finds its next tile resident when it gets there, while
+// the two teams' compute and store phases interleave on the SM -- the load
+// latency the two-CTA layout exposes is hidden without a fourth buffer.
+// Within a team the register-group code and every reduction order are those
+// of pass_kernel (team-local named barriers instead of __syncthreads), so the
+// results are bitwise identical.
+__device__ __forceinline__ void team_sync(int team) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "r"(256) : "memory");
+}
+__device__ __forceinline__ double team_sum(double v, double* sred, int team, int t) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    team_sync(team);
+    if ((t & 31) == 0) sred[t >> 5] = v;
+    team_sync(team);
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += sred[w];
+    return s;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+// arrives once this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+
+template <typename T, int MODE>   // MODE 1: store (F_STORE / F_NORM / F_SUPPORT), 2: shift pair (F_PAIR)
+__global__ void __launch_bounds__(512, 1)
+ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent,
+                 int nstates, int unused, EpiArgs ep) {
+    typedef typename Cx<T>::V V;
+    constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
+    constexpr int NA = 1 << R;
+    constexpr int TB = 8;                       // 256 threads per team
+    constexpr int K = TB + R;
+    constexpr size_t TILE = sizeof(V) << K;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + 3 * TILE);              // 3 mbarriers
+    double* sred_all = reinterpret_cast<double*>(full + 4);                          // 2 x 8
+    GroupDesc* sg = reinterpret_cast<GroupDesc*>(sred_all + 16);
+    V* smat_all = reinterpret_cast<V*>(sg + pd.ng);                                  // 2 x nm x 4
+    (void)unused;
+
+    const int team = threadIdx.x >> 8;
+    const int t = threadIdx.x & 255;
+    double* sred = sred_all + 8 * team;
+    V* smat = smat_all + (size_t)team * pd.nm * 4;
+    const int64_t ntiles = ep.ntiles;
+    const int64_t items = ntiles * nstates;
+    const int64_t G = gridDim.x;
+    const int64_t c = blockIdx.x;
+    {
+        const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
+        uint4* gdst = reinterpret_cast<uint4*>(sg);
+        for (int i = threadIdx.x; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
+        if (threadIdx.x < 3) mbar_init(full + threadIdx.x, 256);
+    }
+    __syncthreads();
+    uint32_t tslot = 0, fslot = 0;
+    uint64_t tg = 0;
+#pragma unroll
+    for (int j = 0; j < TB; ++j)
+        if ((t >> j) & 1) { tslot ^= pd.swz[j]; fslot ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
+    auto outer_of = [&](int64_t x) {
+        uint64_t o = 0;
+        for (int j = 0; j < pd.n_outer; ++j)
+            if ((x >> j) & 1) o |= 1ull << pd.obits[j];
+        return o;
+    };
+    auto load_src = [&](int64_t w) -> const V* {
+        const V* in = reinterpret_cast<const V*>(ent[w % nstates].in);
+        return in == nullptr ? nullptr : in + (outer_of(w / nstates) | tg);
+    };
+    // this thread's share of item i's tile -> buffer i % 3, then one arrival
+    auto load_item = [&](const V* src, int64_t i) {
+        unsigned char* dst = smem_raw + (size_t)(i % 3) * TILE;
+        if (src != nullptr) {
+#pragma unroll
+            for (int it = 0; it < NA; ++it)
+                cp_async<sizeof(V)>(dst + (size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V), src + pd.g_hi[it]);
+        }
+        mbar_arrive_cp_async(full + i % 3);
+    };
+    // prologue: item i's load is issued by team (i + 1) mod 2 (the team of item i - 3)
+    for (int64_t i = 0; i < 3; ++i)
+        if (c + i * G < items && (int)((i + 1) & 1) == team) load_item(load_src(c + i * G), i);
+
+    int cur_y = -1;
+    LaunchEntry e;
+    for (int64_t i = team; c + i * G < items; i += 2) {
+        const int64_t w = c + i * G;
+        const int y = (int)(w % nstates);
+        const int64_t x = w / nstates;
+        unsigned char* tileb = smem_raw + (size_t)(i % 3) * TILE;
+        if (y != cur_y) {
+            e = ent[y];
+            const V* msrc = reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4;
+            for (int q = t; q < pd.nm * 4; q += 256) smat[q] = msrc[q];
+            cur_y = y;
+        }
+        const bool gen = e.in == nullptr;
+        V* __restrict__ out = reinterpret_cast<V*>(e.out);
+        const bool store = (ep.flags & F_STORE) && out != nullptr;
+        const uint64_t outer = outer_of(x);
+        const bool zero_tile = gen && x != 0;
+        mbar_wait(full + i % 3, (unsigned)((i / 3) & 1));   // this item's tile has landed
+        if (gen) {
+#pragma unroll
+            for (int it = 0; it < NA; ++it) {
+                V v;
+                v.x = (x == 0 && t == 0 && it == 0) ? T(1) : T(0);
+                v.y = T(0);
+                *reinterpret_cast<V*>(tileb + ((size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V))) = v;
+            }
+        }
+        team_sync(team);
+        // ---- register groups (as pass_kernel) --------------------------------
+        if (!zero_tile) {
+            const uint32_t boff = (uint32_t)(tileb - smem_raw);
+            for (int g = 0; g < pd.ng; ++g) {
+                const GroupDesc& GD = sg[g];
+                const int4 mats = *reinterpret_cast<const int4*>(GD.mat);
+                V m00, m01, m10, m11;
+                if (mats.x >= 0) {
+                    const V* M = smat + mats.x * 4;
+                    m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
+                }
+                uint32_t base = boff;
+#pragma unroll
+                for (int m = 0; m < TB; ++m)
+                    if ((t >> m) & 1) base ^= GD.tcol[m];
+                uint32_t off[NA];
+#pragma unroll
+                for (int q = 0; q < NA / 4; ++q) {
+                    const uint4 cc = reinterpret_cast<const uint4*>(GD.combo)[q];
+                    off[4 * q] = base ^ cc.x;
+                    off[4 * q + 1] = base ^ cc.y;
+                    off[4 * q + 2] = base ^ cc.z;
+                    off[4 * q + 3] = base ^ cc.w;
+                }
+                V a[NA];
+#pragma unroll
+                for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off[j]);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
+                    if (mi >= 0) {
+                        if (r > 0) {
+                            const V* M = smat + mi * 4;
+                            m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
+                        }
+#pragma unroll
+                        for (int j = 0; j < NA; ++j)
+                            if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off[j]) = a[j];
+                if (g + 1 < pd.ng && !sg[g + 1].cta_sync) __syncwarp();
+                else team_sync(team);
+            }
+        }
+        // ---- store / reduce: every shared-memory read before the team barrier
+        const V* next_src = (c + (i + 3) * G < items) ? load_src(c + (i + 3) * G) : nullptr;
+        double acc = 0.0;
+        V vals[NA];
+        if (MODE == 1 && (ep.flags & F_SUPPORT)) {
+            const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
+            double* row = ep.sup_out + e.rslot * (ep.S + 1);
+            for (int32_t q = lo + t; q < hi; q += 256) {
+                const uint32_t slot = apply_cols(pd.fin, K, (uint32_t)ep.sup_local[q]);
+                row[ep.sup_pos[q]] = norm2(*reinterpret_cast<const V*>(tileb + (size_t)slot * sizeof(V)));
+            }
+        }
+        if (MODE == 2) {
+            const V* __restrict__ aux = reinterpret_cast<const V*>(e.aux);
+            double accB = 0.0, accC = 0.0;
+            const V* __restrict__ src = aux + (outer | tg);
+#pragma unroll
+            for (int it = 0; it < NA; ++it) {
+                const V v = *reinterpret_cast<const V*>(tileb + (size_t)(fslot ^ pd.fin_hi[it]) * sizeof(V));
+                const V u = __ldcs(src + pd.g_hi[it]);
+                acc += norm2(u);
+                accB += norm2(v);
+                accC += (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+            }
+            const double A = team_sum(acc, sred, team, t);
+            const double B = team_sum(accB, sred, team, t);
+            const double C = team_sum(accC, sred, team, t);
+            if (t == 0) {
+                double* p = ep.partial + (e.pslot * ntiles + x) * 3;
+                p[0] = A;
+                p[1] = B;
+                p[2] = C;
+            }
+            const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
+            for (int32_t q = lo + t; q < hi; q += 256) {
+                const uint32_t loc = (uint32_t)ep.sup_local[q];
+                const V v = *reinterpret_cast<const V*>(tileb + (size_t)apply_cols(pd.fin, K, loc) * sizeof(V));
+                uint64_t gidx = outer;
+                for (int j = 0; j < K; ++j)
+                    if ((loc >> j) & 1u) gidx |= 1ull << pd.sbits[j];
+                const V u = aux[gidx];
+                double* row = ep.pair_sup + (e.rslot * ep.S + ep.sup_pos[q]) * 3;
+                row[0] = norm2(u);
+                row[1] = norm2(v);
+                row[2] = (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+            }
+        } else {
+#pragma unroll
+            for (int it = 0; it < NA; ++it) {
+                vals[it] = *reinterpret_cast<const V*>(tileb + (size_t)(fslot ^ pd.fin_hi[it]) * sizeof(V));
+                acc += norm2(vals[it]);
+            }
+        }
+        team_sync(team);   // the buffer is drained: item i + 3 streams into it
+        if (c + (i + 3) * G < items) load_item(next_src, i + 3);
+        if (MODE == 1 && store) {
+            V* __restrict__ dst = out + (outer | tg);
+#pragma unroll
+            for (int it = 0; it < NA; ++it) __stcs(dst + pd.g_hi[it], vals[it]);
+        }
+        if (MODE == 1 && (ep.flags & F_NORM)) {
+            const double s = team_sum(acc, sred, team, t);
+            if (t == 0) ep.partial[e.pslot * ntiles + x] = s;
+        }
+    }
+    cp_async_wait<0>();   // loads issued for the other team complete before this thread exits
 }
 
 // Multi-tile norm / support finalisation: one CTA per result slot.

@@ -295,12 +295,29 @@ PassFn<T> pass_kernel_multi(bool pair) {
                 : &pass_kernel<T, multi_tile_tb<T>(), multi_tile_db<T>(), 1>;
 }
 
+// Ring kernel (two teams, three buffers, one CTA per SM) for complex128
+// multi-tile passes.  Off by default: measured on B200 it hides the load
+// latency but ran the 28q gradient 5% slower than two independent CTAs per SM
+// (45.3 s vs 43.0 s); QV_RING=1 selects it for experiments.
+#ifndef QV_RING
+#define QV_RING 0
+#endif
+template <typename T>
+constexpr bool use_ring() { return QV_RING && sizeof(T) == 8 && multi_tile_tb<T>() == 8; }
+template <typename T>
+PassFn<T> ring_kernel(bool pair) {
+    return pair ? &ring_pass_kernel<T, 2> : &ring_pass_kernel<T, 1>;
+}
+
 template <typename T>
 void set_kernel_attributes() {
     for (auto fn : pass_kernels<T>())
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    for (bool pair : {false, true})
+    for (bool pair : {false, true}) {
         CK(cudaFuncSetAttribute(pass_kernel_multi<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        if (use_ring<T>())
+            CK(cudaFuncSetAttribute(ring_kernel<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    }
 }
 
 template <typename T>
@@ -309,11 +326,16 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     typedef typename Cx<T>::V V;
     const int tb = pd.k - reg_bits(sizeof(T) == 8 ? 0 : 1);
     const bool multi = ntiles > 1 && tb == multi_tile_tb<T>();
-    const bool db = multi && multi_tile_db<T>();
-    const size_t smem = (sizeof(V) << pd.k) * (db ? 2 : 1) + (size_t)pd.ng * sizeof(GroupDesc) +
-                        (size_t)pd.nm * 4 * sizeof(V) + 32 * sizeof(double);
-    const int threads = pass_threads(tb);
-    PassFn<T> fn = multi ? pass_kernel_multi<T>((ep.flags & F_PAIR) != 0) : pass_kernels<T>()[tb];
+    const bool ring = multi && use_ring<T>();
+    const bool db = multi && !ring && multi_tile_db<T>();
+    const size_t smem = ring ? (sizeof(V) << pd.k) * 3 + 32 + 16 * sizeof(double) + (size_t)pd.ng * sizeof(GroupDesc) +
+                                   (size_t)pd.nm * 8 * sizeof(V)
+                             : (sizeof(V) << pd.k) * (db ? 2 : 1) + (size_t)pd.ng * sizeof(GroupDesc) +
+                                   (size_t)pd.nm * 4 * sizeof(V) + 32 * sizeof(double) + (multi ? 8192 : 0);
+    const int threads = ring ? 512 : pass_threads(tb);
+    PassFn<T> fn = ring    ? ring_kernel<T>((ep.flags & F_PAIR) != 0)
+                   : multi ? pass_kernel_multi<T>((ep.flags & F_PAIR) != 0)
+                           : pass_kernels<T>()[tb];
     // persistent CTAs: enough per state to fill every SM at full occupancy
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
@@ -330,7 +352,9 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     // first launch with >= 8 items per CTA; written to $QVB200_TRACE_OUT
     static bool traced = false;
     long long* d_trace = nullptr;
-    const bool do_trace = !traced && pd.m0 > 0 && ntiles * nstates >= 8 * blocks && getenv("QVB200_TRACE_OUT");
+    const char* min_m0 = getenv("QVB200_TRACE_MIN_M0");   // trace a later pass (matrix slot >= value)
+    const bool do_trace = !traced && pd.m0 > 0 && pd.m0 >= (min_m0 ? atoi(min_m0) : 0) &&
+                          ntiles * nstates >= 8 * blocks && getenv("QVB200_TRACE_OUT");
     if (do_trace) {
         CK(cudaMalloc(&d_trace, 8 * 64 * 16 * sizeof(long long)));
         CK(cudaMemsetAsync(d_trace, 0, 8 * 64 * 16 * sizeof(long long), E.stream));

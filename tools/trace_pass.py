@@ -44,7 +44,9 @@ def main():
             if not v.any():
                 continue
             line.append(f"{name}:{int(np.median(v) - t0)}[{int(v.min() - t0)},{int(v.max() - t0)}]")
-        print(f"item {item}: " + "  ".join(line))
+        nxt = tr[item + 1, 0, :warps] if item + 1 < 8 else None
+        gap = f"  next item +{int(nxt[nxt > 0].min() - t0)}" if nxt is not None and nxt.any() else ""
+        print(f"item {item}: " + "  ".join(line) + gap)
 
 
 if __name__ == "__main__":
