@@ -160,7 +160,12 @@ template <typename T, int TB, bool DB, int MODE>
 #ifndef QV_TB9_MIN_BLOCKS
 #define QV_TB9_MIN_BLOCKS 1
 #endif
-__global__ void __launch_bounds__(pass_threads(TB), (DB ? 1 : TB >= 9 ? QV_TB9_MIN_BLOCKS : TB == 8 ? 2 : 4))
+#ifndef QV_C64_TB8_MIN_BLOCKS
+#define QV_C64_TB8_MIN_BLOCKS 3   // complex64 at 12 tile bits: three CTAs per SM (<= 85 registers)
+#endif
+__global__ void __launch_bounds__(pass_threads(TB), (DB ? (sizeof(T) == 4 && TB == 8 ? QV_C64_TB8_MIN_BLOCKS : 1)
+                                                     : TB >= 9 ? QV_TB9_MIN_BLOCKS
+                                                     : TB == 8 ? (sizeof(T) == 4 ? QV_C64_TB8_MIN_BLOCKS : 2) : 4))
 pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent,
             int nstates, int unused, EpiArgs ep) {
     typedef typename Cx<T>::V V;
@@ -181,8 +186,8 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
 
     const int tid = threadIdx.x;
     const int64_t ntiles = ep.ntiles;
-    const int64_t items = ntiles * nstates;
-    const int64_t G = gridDim.x;
+    const int items = (int)(ntiles * nstates);   // < 2^31 (host-checked)
+    const int G = gridDim.x;
     {   // stage the pass's group descriptors (once per CTA)
         const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
         uint4* gdst = reinterpret_cast<uint4*>(sg);
@@ -205,7 +210,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
 #pragma unroll
     for (int j = 0; j < TB; ++j)
         if ((tid >> j) & 1) { tslot ^= pd.swz[j]; fslot ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
-    auto outer_of = [&](int64_t x) -> uint64_t {
+    auto outer_of = [&](int x) -> uint64_t {
         if constexpr (MT) {
             return otab[x & 255] | otab[256 + ((x >> 8) & 255)] | otab[512 + ((x >> 16) & 255)] |
                    otab[768 + ((x >> 24) & 255)];
@@ -217,30 +222,37 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         }
     };
     // item w = x * nstates + y (state fastest); CTA items advance by G = gx * nstates + gy
-    const int64_t gx = G / nstates;
+    const int gx = G / nstates;
     const int gy = (int)(G % nstates);
-    auto src_of = [&](int64_t xx, int yy) -> const V* {   // this thread's first source amplitude of an item
+    auto src_of = [&](int xx, int yy) -> const V* {   // this thread's first source amplitude of an item
         const V* in = reinterpret_cast<const V*>(ent[yy].in);
         return (in == nullptr || !active) ? nullptr : in + (outer_of(xx) | tg);
     };
-    auto load_src = [&](int64_t w) -> const V* { return src_of(w / nstates, (int)(w % nstates)); };
+    auto load_src = [&](int w) -> const V* { return src_of(w / nstates, w % nstates); };
+    // slots whose local index has a `fresh` bit hold amplitudes no earlier
+    // pass wrote (exactly zero): they are zero-filled instead of loaded
+    const bool t_fresh = (tid & pd.fresh) != 0;
+    const uint32_t hi_fresh = pd.fresh >> TB;
     auto issue_from = [&](const V* src, unsigned char* dst) {   // NA async 8/16-byte copies per thread
         if (src == nullptr) return;
 #pragma unroll
-        for (int it = 0; it < NA; ++it)
-            cp_async<sizeof(V)>(dst + (size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V), src + pd.g_hi[it]);
+        for (int it = 0; it < NA; ++it) {
+            unsigned char* d = dst + (size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V);
+            if (t_fresh || (it & hi_fresh)) *reinterpret_cast<V*>(d) = V{T(0), T(0)};
+            else cp_async<sizeof(V)>(d, src + pd.g_hi[it]);
+        }
     };
-    auto issue_load = [&](int64_t w, unsigned char* dst) { issue_from(load_src(w), dst); };
+    auto issue_load = [&](int w, unsigned char* dst) { issue_from(load_src(w), dst); };
     if (blockIdx.x < items) issue_load(blockIdx.x, smem_raw);
     cp_async_commit();
 
     int cur_y = -1;
     LaunchEntry e;
-    int64_t i = 0;
-    int64_t x = (int64_t)blockIdx.x / nstates;
-    int y = (int)((int64_t)blockIdx.x % nstates);
-    for (int64_t w = blockIdx.x; w < items; w += G, ++i) {
-        int64_t xn = x + gx;   // the next item's coordinates
+    int i = 0;
+    int x = (int)blockIdx.x / nstates;
+    int y = (int)blockIdx.x % nstates;
+    for (int w = blockIdx.x; w < items; w += G, ++i) {
+        int xn = x + gx;   // the next item's coordinates
         int yn = y + gy;
         if (yn >= nstates) { yn -= nstates; ++xn; }
         QV_MARK(0);
@@ -547,7 +559,8 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + 3 * TILE);              // 3 mbarriers
     double* sred_all = reinterpret_cast<double*>(full + 4);                          // 2 x 8
-    GroupDesc* sg = reinterpret_cast<GroupDesc*>(sred_all + 16);
+    uint64_t* otab = reinterpret_cast<uint64_t*>(sred_all + 16);                     // 4 x 256 outer offsets
+    GroupDesc* sg = reinterpret_cast<GroupDesc*>(otab + 1024);
     V* smat_all = reinterpret_cast<V*>(sg + pd.ng);                                  // 2 x nm x 4
     (void)unused;
 
@@ -556,14 +569,21 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
     double* sred = sred_all + 8 * team;
     V* smat = smat_all + (size_t)team * pd.nm * 4;
     const int64_t ntiles = ep.ntiles;
-    const int64_t items = ntiles * nstates;
-    const int64_t G = gridDim.x;
-    const int64_t c = blockIdx.x;
+    const int items = (int)(ntiles * nstates);   // < 2^31 (host-checked)
+    const int G = gridDim.x;
+    const int c = blockIdx.x;
     {
         const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
         uint4* gdst = reinterpret_cast<uint4*>(sg);
         for (int i = threadIdx.x; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
         if (threadIdx.x < 3) mbar_init(full + threadIdx.x, 256);
+        for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+            const int b = idx >> 8, v = idx & 255;
+            uint64_t o = 0;
+            for (int j = 0; j < 8; ++j)
+                if (((v >> j) & 1) && 8 * b + j < pd.n_outer) o |= 1ull << pd.obits[8 * b + j];
+            otab[idx] = o;
+        }
     }
     __syncthreads();
     uint32_t tslot = 0, fslot = 0;
@@ -571,36 +591,42 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
 #pragma unroll
     for (int j = 0; j < TB; ++j)
         if ((t >> j) & 1) { tslot ^= pd.swz[j]; fslot ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
-    auto outer_of = [&](int64_t x) {
-        uint64_t o = 0;
-        for (int j = 0; j < pd.n_outer; ++j)
-            if ((x >> j) & 1) o |= 1ull << pd.obits[j];
-        return o;
+    auto outer_of = [&](int x) -> uint64_t {
+        return otab[x & 255] | otab[256 + ((x >> 8) & 255)] | otab[512 + ((x >> 16) & 255)] |
+               otab[768 + ((x >> 24) & 255)];
     };
-    auto load_src = [&](int64_t w) -> const V* {
-        const V* in = reinterpret_cast<const V*>(ent[w % nstates].in);
-        return in == nullptr ? nullptr : in + (outer_of(w / nstates) | tg);
+    auto src_of = [&](int xx, int yy) -> const V* {
+        const V* in = reinterpret_cast<const V*>(ent[yy].in);
+        return in == nullptr ? nullptr : in + (outer_of(xx) | tg);
     };
+    auto load_src = [&](int w) -> const V* { return src_of(w / nstates, w % nstates); };
+    // item coordinates advance by multiples of G: (x, y) += (kG / nstates, kG % nstates) with carry
+    const int g2x = 2 * G / nstates, g3x = 3 * G / nstates;
+    const int g2y = 2 * G % nstates, g3y = 3 * G % nstates;
     // this thread's share of item i's tile -> buffer i % 3, then one arrival
-    auto load_item = [&](const V* src, int64_t i) {
+    const bool t_fresh = (t & pd.fresh) != 0;   // zero-filled slots (see pass_kernel)
+    const uint32_t hi_fresh = pd.fresh >> TB;
+    auto load_item = [&](const V* src, int i) {
         unsigned char* dst = smem_raw + (size_t)(i % 3) * TILE;
         if (src != nullptr) {
 #pragma unroll
-            for (int it = 0; it < NA; ++it)
-                cp_async<sizeof(V)>(dst + (size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V), src + pd.g_hi[it]);
+            for (int it = 0; it < NA; ++it) {
+                unsigned char* d = dst + (size_t)(tslot ^ pd.swz_hi[it]) * sizeof(V);
+                if (t_fresh || (it & hi_fresh)) *reinterpret_cast<V*>(d) = V{T(0), T(0)};
+                else cp_async<sizeof(V)>(d, src + pd.g_hi[it]);
+            }
         }
         mbar_arrive_cp_async(full + i % 3);
     };
     // prologue: item i's load is issued by team (i + 1) mod 2 (the team of item i - 3)
-    for (int64_t i = 0; i < 3; ++i)
-        if (c + i * G < items && (int)((i + 1) & 1) == team) load_item(load_src(c + i * G), i);
+    for (int i = 0; i < 3; ++i)
+        if (c + i * G < items && ((i + 1) & 1) == team) load_item(load_src(c + i * G), i);
 
     int cur_y = -1;
     LaunchEntry e;
-    for (int64_t i = team; c + i * G < items; i += 2) {
-        const int64_t w = c + i * G;
-        const int y = (int)(w % nstates);
-        const int64_t x = w / nstates;
+    int x = (c + team * G) / nstates;
+    int y = (c + team * G) % nstates;
+    for (int i = team; c + i * G < items; i += 2) {
         unsigned char* tileb = smem_raw + (size_t)(i % 3) * TILE;
         if (y != cur_y) {
             e = ent[y];
@@ -671,7 +697,10 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
             }
         }
         // ---- store / reduce: every shared-memory read before the team barrier
-        const V* next_src = (c + (i + 3) * G < items) ? load_src(c + (i + 3) * G) : nullptr;
+        int x3 = x + g3x;   // item i + 3 (loaded by this team for the other one)
+        int y3 = y + g3y;
+        if (y3 >= nstates) { y3 -= nstates; ++x3; }
+        const V* next_src = (c + (i + 3) * G < items) ? src_of(x3, y3) : nullptr;
         double acc = 0.0;
         V vals[NA];
         if (MODE == 1 && (ep.flags & F_SUPPORT)) {
@@ -734,6 +763,9 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
             const double s = team_sum(acc, sred, team, t);
             if (t == 0) ep.partial[e.pslot * ntiles + x] = s;
         }
+        x += g2x;   // this team's next item, i + 2
+        y += g2y;
+        if (y >= nstates) { y -= nstates; ++x; }
     }
     cp_async_wait<0>();   // loads issued for the other team complete before this thread exits
 }

@@ -32,14 +32,21 @@ constexpr int kGroupAmps = 1 << kRegBits;
 __host__ __device__
 #endif
 constexpr int reg_bits(int precision) { return precision == 0 ? QV_C128_REG_BITS : 4; }
-// widest tile (multi-tile registers): 2^12 complex128 / 2^13 complex64 = 64 KiB
+// Widest tile (multi-tile registers): 2^12 amplitudes for both precisions
+// (64 KiB complex128, 32 KiB complex64).  Measured on B200: complex128 at 13
+// bits (128 KiB, one CTA per SM) and 11 bits (more passes) are slower; for
+// complex64, 12 bits with three CTAs per SM beat 13 bits with one (32q x 4L
+// gradient 9.6 s vs 10.1 s).
 #ifndef QV_C128_TILE_BITS
 #define QV_C128_TILE_BITS 12
+#endif
+#ifndef QV_C64_TILE_BITS
+#define QV_C64_TILE_BITS 12
 #endif
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-constexpr int max_tile_bits(int precision) { return precision == 0 ? QV_C128_TILE_BITS : 13; }
+constexpr int max_tile_bits(int precision) { return precision == 0 ? QV_C128_TILE_BITS : QV_C64_TILE_BITS; }
 constexpr int kMaxTileBits = 13;     // 2^13 amplitudes (64 KiB at complex64, 128 KiB c128)
 constexpr int kMaxQubits = 40;
 
@@ -90,7 +97,8 @@ struct alignas(16) PassDesc {
     int32_t n_outer;     // n - k outer (tile-index) bits
     int32_t g0, ng;      // group range in the plan's group array
     int32_t m0, nm;      // matrix slot range in a circuit's matrix table
-    int32_t pad0, pad1;
+    uint32_t fresh;      // logical local bits no earlier pass touched: amplitudes there are 0, loaded as zeros
+    int32_t pad1;
     uint8_t sbits[16];   // logical local bit j -> global index bit
     uint8_t obits[40];   // outer bit j -> global index bit
     uint16_t swz[16];    // physical slot column of logical bit j at load time

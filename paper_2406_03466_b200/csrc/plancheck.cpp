@@ -136,6 +136,25 @@ int qvp_plan_stats(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* 
     }
 }
 
+// Raw device descriptors of a plan: groups (128 B each) and passes
+// (sizeof(PassDesc) each).  Returns the group count; *n_passes gets the pass count.
+int qvp_plan_descriptors(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                         int precision, int max_tile_bits, void* groups, int32_t group_cap, void* passes,
+                         int32_t pass_cap, int32_t* n_passes) {
+    try {
+        const Topology topo = make_topo(n, n_gates, kinds, q0, q1);
+        const Plan plan = build_plan(topo, precision, max_tile_bits);
+        if ((int32_t)plan.groups.size() <= group_cap)
+            std::memcpy(groups, plan.groups.data(), plan.groups.size() * sizeof(GroupDesc));
+        if ((int32_t)plan.pdesc.size() <= pass_cap)
+            std::memcpy(passes, plan.pdesc.data(), plan.pdesc.size() * sizeof(PassDesc));
+        *n_passes = (int32_t)plan.pdesc.size();
+        return (int)plan.groups.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // Tile bit set of every pass as a bit mask (global index bits).
 int qvp_plan_pass_masks(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
                         int precision, int max_tile_bits, uint64_t* masks, int32_t cap) {

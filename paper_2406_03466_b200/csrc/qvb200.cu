@@ -328,7 +328,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const bool multi = ntiles > 1 && tb == multi_tile_tb<T>();
     const bool ring = multi && use_ring<T>();
     const bool db = multi && !ring && multi_tile_db<T>();
-    const size_t smem = ring ? (sizeof(V) << pd.k) * 3 + 32 + 16 * sizeof(double) + (size_t)pd.ng * sizeof(GroupDesc) +
+    const size_t smem = ring ? (sizeof(V) << pd.k) * 3 + 32 + 16 * sizeof(double) + 8192 + (size_t)pd.ng * sizeof(GroupDesc) +
                                    (size_t)pd.nm * 8 * sizeof(V)
                              : (sizeof(V) << pd.k) * (db ? 2 : 1) + (size_t)pd.ng * sizeof(GroupDesc) +
                                    (size_t)pd.nm * 4 * sizeof(V) + 32 * sizeof(double) + (multi ? 8192 : 0);
@@ -344,6 +344,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E.device));
     const int64_t slots = (int64_t)per_sm * sms;
     const int64_t blocks = std::min<int64_t>(ntiles * nstates, slots);   // exactly one persistent wave
+    if (ntiles * nstates + 4 * blocks >= (1ll << 31)) throw ArgError("launch has too many (state, tile) items");
     EpiArgs e2 = ep;
     e2.ntiles = ntiles;
     e2.trace = nullptr;
@@ -389,44 +390,71 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     E.stats[11] += (double)nstates * amps * 14.0 * pd.nm;
 }
 
-// Backward light cone of a support-restricted output (SUPPORT / JS results).
-// A bit that is zero in every support index and that no pass from p on
-// touches is a spectator: the final amplitudes on the support only depend on
-// the inputs of pass p whose spectator bits are zero.  cone[p] = the bits
-// pass p must range over (support bits | tile bits of passes p..P-1); pass p
-// then runs on 2^|outer bits in cone[p]| tiles instead of all of them.  For the
-// QCL benchmarks (support = the 2^10 low indices) the last passes of every
-// circuit touch 1, 4, 1024 tiles instead of 2^16.
-std::vector<uint64_t> support_cone(const Plan& plan, const uint64_t* support, int64_t S) {
+// Light cone of a support-restricted output (SUPPORT / JS results, shift
+// pairs).  Backward: a bit that is zero in every support index and that no
+// pass from p on touches is a spectator -- the final amplitudes on the support
+// only depend on the inputs of pass p whose spectator bits are zero, so
+// cone[p] = support bits | tile bits of passes p..P-1.  Forward: every state
+// starts as |0...0>, so before pass p only the bits some earlier pass touched
+// (seen[p]) can be nonzero.  Pass p then runs on the tiles whose outer bits
+// outside cone[p] & seen[p] are zero, and zero-fills the local slots of bits
+// it is the first to touch (`fresh`) instead of loading them.  For the QCL
+// benchmarks the first two passes touch 1 and 256 tiles and the last three 1,
+// 4 and 1024 tiles of 2^16.  Support indices with a bit no pass touches have
+// probability exactly 0 (`reach` excludes them).
+struct LightCone {
+    std::vector<uint64_t> outer_free;   // per pass: global bits the tile index ranges over
+    std::vector<uint32_t> fresh;        // per pass: logical local bits loaded as zeros
+    uint64_t reach = 0;                 // bits any pass touches
+};
+LightCone light_cone(const Plan& plan, const uint64_t* support, int64_t S) {
+    const size_t P = plan.passes.size();
+    LightCone lc;
+    lc.outer_free.resize(P);
+    lc.fresh.resize(P);
     uint64_t acc = 0;
     for (int64_t s = 0; s < S; ++s) acc |= support[s];
-    std::vector<uint64_t> cone(plan.passes.size());
-    for (size_t p = plan.passes.size(); p-- > 0;) {
+    std::vector<uint64_t> cone(P);
+    for (size_t p = P; p-- > 0;) {
         for (int b : plan.passes[p].S) acc |= 1ull << b;
         cone[p] = acc;
     }
-    return cone;
+    uint64_t seen = 0;
+    for (size_t p = 0; p < P; ++p) {
+        lc.outer_free[p] = cone[p] & seen;
+        uint32_t fresh = 0;
+        for (size_t j = 0; j < plan.passes[p].S.size(); ++j)
+            if (!((seen >> plan.passes[p].S[j]) & 1)) fresh |= 1u << j;
+        lc.fresh[p] = fresh;
+        for (int b : plan.passes[p].S) seen |= 1ull << b;
+    }
+    lc.reach = seen;
+    return lc;
 }
 
-// The pass restricted to the tiles whose outer bits outside `cone` are zero.
-PassDesc restrict_pass(const PassDesc& pd, uint64_t cone) {
+// The pass restricted to the tiles whose outer bits outside `free` are zero.
+PassDesc restrict_pass(const PassDesc& pd, uint64_t free, uint32_t fresh) {
     PassDesc r = pd;
     int m = 0;
     for (int j = 0; j < pd.n_outer; ++j)
-        if ((cone >> pd.obits[j]) & 1) r.obits[m++] = pd.obits[j];
+        if ((free >> pd.obits[j]) & 1) r.obits[m++] = pd.obits[j];
     for (int j = m; j < (int)sizeof(r.obits); ++j) r.obits[j] = 0;
     r.n_outer = m;
+    r.fresh = fresh;
     return r;
 }
 
 // Support indices bucketed by the tile of the last pass that holds them
 // (CSR over tiles) with their logical local index inside the tile; sets
 // ep.sup_off / sup_local / sup_pos.  Requires ep.S and ep.ntiles.
-void upload_support_csr(Engine& E, const PassDesc& last, const uint64_t* support, EpiArgs& ep) {
+// Indices with a bit outside `reach` are left out (their amplitude is 0).
+void upload_support_csr(Engine& E, const PassDesc& last, const uint64_t* support, EpiArgs& ep,
+                        uint64_t reach = ~0ull) {
     const int64_t ntiles = ep.ntiles, S = ep.S;
-    std::vector<int32_t> cnt(ntiles + 1, 0), local(S), tile_of(S);
+    std::vector<int32_t> cnt(ntiles + 1, 0), local(S), tile_of(S, -1);
     for (int64_t s = 0; s < S; ++s) {
         const uint64_t g = support[s];
+        if (g & ~reach) continue;
         uint32_t loc = 0;
         uint64_t tl = 0;
         for (int j = 0; j < last.k; ++j)
@@ -440,6 +468,7 @@ void upload_support_csr(Engine& E, const PassDesc& last, const uint64_t* support
     for (int64_t t = 0; t < ntiles; ++t) cnt[t + 1] += cnt[t];
     std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1), sl(S), sp(S);
     for (int64_t s = 0; s < S; ++s) {
+        if (tile_of[s] < 0) continue;
         const int32_t at = fill[tile_of[s]]++;
         sl[at] = local[s];
         sp[at] = (int32_t)s;
@@ -448,8 +477,10 @@ void upload_support_csr(Engine& E, const PassDesc& last, const uint64_t* support
     int32_t* dloc = E.d_sup_local.get(S);
     int32_t* dpos = E.d_sup_pos.get(S);
     h2d(E, doff, cnt.data(), (ntiles + 1) * 4);
-    h2d(E, dloc, sl.data(), S * 4);
-    h2d(E, dpos, sp.data(), S * 4);
+    if (S > 0) {
+        h2d(E, dloc, sl.data(), S * 4);
+        h2d(E, dpos, sp.data(), S * 4);
+    }
     ep.sup_off = doff;
     ep.sup_local = dloc;
     ep.sup_pos = dpos;
@@ -583,16 +614,22 @@ void GroupRun::run() {
         // the state norm is then not swept (unitary circuits keep it at 1)
         std::vector<PassDesc> rpd(plan.pdesc.begin(), plan.pdesc.end());
         std::vector<int64_t> rtiles(P, ntiles);
+        uint64_t reach = ~0ull;
         if (dist) {
-            const std::vector<uint64_t> cone = support_cone(plan, R->support, ep.S);
+            const LightCone lc = light_cone(plan, R->support, ep.S);
             for (int p = 0; p < P; ++p) {
-                rpd[p] = restrict_pass(plan.pdesc[p], cone[p]);
+                rpd[p] = restrict_pass(plan.pdesc[p], lc.outer_free[p], lc.fresh[p]);
                 rtiles[p] = 1ll << rpd[p].n_outer;
             }
+            reach = lc.reach;
         }
         const bool unit_norm = rtiles[P - 1] < ntiles;
         ep.ntiles = rtiles[P - 1];
-        if (ep.S > 0) upload_support_csr(E, rpd[P - 1], R->support, ep);
+        if (ep.S > 0) {
+            upload_support_csr(E, rpd[P - 1], R->support, ep, reach);
+            // support indices outside the reach are never written: zero rows first
+            CK(cudaMemsetAsync(ep.sup_out, 0, (size_t)U * (ep.S + 1) * sizeof(double), E.stream));
+        }
         const bool need_state_out = !dist;   // Pauli / full read the stored state
 
         // pass signatures per unique state
@@ -944,17 +981,15 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     ep.n = n;
     ep.S = R->support_count;
     const int64_t ntiles = 1ll << (n - plan.k);
-    // every pass on the support's light cone (see support_cone); the norms
+    // every pass on the support's light cone (see light_cone); the norms
     // of Psi0 and Xi are then 1 and Im<Psi0|Xi> = 0 exactly (psi+- = (Psi0 -+
     // i Xi)/sqrt2 are both unit vectors), instead of being swept
     std::vector<PassDesc> rpd(P);
     std::vector<int64_t> rtiles(P);
-    {
-        const std::vector<uint64_t> cone = support_cone(plan, R->support, ep.S);
-        for (int p = 0; p < P; ++p) {
-            rpd[p] = restrict_pass(plan.pdesc[p], cone[p]);
-            rtiles[p] = 1ll << rpd[p].n_outer;
-        }
+    const LightCone lc = light_cone(plan, R->support, ep.S);
+    for (int p = 0; p < P; ++p) {
+        rpd[p] = restrict_pass(plan.pdesc[p], lc.outer_free[p], lc.fresh[p]);
+        rtiles[p] = 1ll << rpd[p].n_outer;
     }
     const bool unit_norm = rtiles[P - 1] < ntiles;
     ep.ntiles = rtiles[P - 1];
@@ -963,7 +998,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     if (ep.S > 0) {
         h2d(E, dsu, R->support, ep.S * 8);
         h2d(E, dta, R->target, ep.S * 8);
-        upload_support_csr(E, rpd[P - 1], R->support, ep);
+        upload_support_csr(E, rpd[P - 1], R->support, ep, lc.reach);
     } else {
         std::vector<int32_t> zeros(ep.ntiles + 1, 0);
         int32_t* doff = E.d_sup_off.get(ep.ntiles + 1);
@@ -973,6 +1008,8 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     ep.support = dsu;
     ep.target = dta;
     ep.pair_sup = E.d_pauli_out.get((size_t)std::max<int64_t>(1, nshift * ep.S * 3));
+    // rows of support indices outside the reach are never written (their amplitude is 0)
+    CK(cudaMemsetAsync(ep.pair_sup, 0, (size_t)std::max<int64_t>(1, nshift * ep.S * 3) * sizeof(double), E.stream));
     double* d_out = E.d_js_out.get((size_t)2 * nshift);
 
     // memory: Psi0 + trunk + W work states

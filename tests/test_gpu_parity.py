@@ -201,3 +201,42 @@ def test_extension_gates_rx_cz_against_oracle(gpu):
         amps = sv.run_gates(n, gates)
         want = 0.7 * sv.pauli_expectation(amps, n, *sv.term_masks(term.factors, n))
         assert got == pytest.approx(want, abs=TOL128), n
+
+
+def test_light_cone_untouched_qubits_and_scattered_support(gpu):
+    """Support-restricted runs sweep only the light cone (forward from |0>,
+    backward from the support).  Qubits 0 and 1 carry no gate (their bits are
+    never in a tile), the support mixes indices inside and outside that
+    reach, and the shifted losses come from the pair path: all against the
+    dense oracle."""
+    n = 15
+    rng = np.random.Generator(np.random.PCG64(77))
+    names = [f"p{i}" for i in range(3 * (n - 2))]
+    it = iter(names)
+    gates = []
+    for q in range(2, n):
+        gates += [qv.h(q), qv.ry(q, next(it))]
+    gates += [qv.cnot(q, q + 1) for q in range(2, n - 1)]
+    for q in range(2, n):
+        gates += [qv.rz(q, next(it)), qv.ry(q, next(it))]
+    tpl = qv.Circuit(n, tuple(gates), name="cone", params=tuple(names))
+    theta = rng.uniform(0, 2 * math.pi, len(names))
+    idx = np.unique(np.concatenate([rng.integers(0, 1 << n, 200), rng.integers(0, 1 << (n - 2), 200)]))
+    w = rng.uniform(0.0, 1.0, idx.size)
+    target = {format(int(i), f"0{n}b"): float(v / w.sum()) for i, v in zip(idx, w)}
+    backend = qv.B200Backend(device=0)
+
+    def oracle_js(values):
+        circ = qv.bind(tpl, values)
+        amps = sv.run_gates(n, [(g.kind.value, g.targets, g.angle) for g in circ.gates])
+        return sv.js_divergence(target, sv.born_distribution(amps, n))
+
+    got = backend.js_losses([qv.bind(tpl, theta)], n, target)[0]
+    assert got == pytest.approx(oracle_js(theta), abs=TOL128)
+    ks = [0, 5, len(names) - 1]
+    pair = backend.shift_js_losses(tpl, theta, target, ks)
+    for j, k in enumerate(ks):
+        for s, sign in enumerate((1.0, -1.0)):
+            shifted = theta.copy()
+            shifted[k] += sign * math.pi / 2
+            assert pair[2 * j + s] == pytest.approx(oracle_js(shifted), abs=TOL128), (k, sign)

@@ -80,7 +80,7 @@ def test_ddcl_layers_multi_pass(plan_lib, n, layers, tile):
 
 @pytest.mark.parametrize("n,layers,precision", [(13, 2, 0), (14, 2, 1), (16, 1, 0), (15, 1, 1)])
 def test_ddcl_production_tiles_and_warp_local_segments(plan_lib, n, layers, precision):
-    """Production tile sizes (k = 12 / 13: 8 / 16 warps).  The interpreter
+    """Production tile sizes (k = 12 for both precisions: 8 warps).  The interpreter
     returns -2 if a group without a CTA barrier makes any warp touch slots
     other than the ones it wrote in the previous group."""
     gates = sv.bind_template(sv.ddcl_template_gates(n, layers), sv.random_angles(6 * n * layers, n))
@@ -104,7 +104,7 @@ def test_random_circuits_multi_warp_tiles(plan_lib, seed):
 
 def test_pass_counts_for_baseline_configs(plan_lib):
     """Regression guard on the planner: HBM sweeps per circuit."""
-    expect_max = {(28, 8): 23, (20, 6): 11, (32, 4): 13}
+    expect_max = {(28, 8): 23, (20, 6): 11, (32, 4): 17}
     for (n, layers), cap in expect_max.items():
         gates = sv.bind_template(sv.ddcl_template_gates(n, layers), [0.1] * (6 * n * layers))
         precision = 1 if n == 32 else 0
