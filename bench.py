@@ -5,7 +5,7 @@ B200, by qubits x layers.  Default workload = config 4, the north star's:
 QCL 28 qubits x 8 layers, complex128, one step = one full parameter-shift
 gradient (2 * 6nL = 2688 circuits), strong scaling over GPUs.
 
-    python bench.py [--gpus N --steps K --warmup W] [--workload qcl28|qcl20|qcl32|qcl4|mcvqe8]
+    python bench.py [--gpus N --steps K --warmup W] [--workload qcl28|qcl20|qcl20fwd|qcl20b|qcl32|qcl4|mcvqe8]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # the reference CPU implementation
 
@@ -41,6 +41,10 @@ WORKLOADS = {
     # name: (kind, n, layers, precision, description)
     "qcl28": ("qcl", 28, 8, "complex128", "config 4: QCL 28 qubits x 8 layers full parameter-shift gradient, complex128"),
     "qcl20": ("qcl", 20, 6, "complex128", "config 3: QCL 20 qubits x 6 layers full gradient for one data point, complex128"),
+    "qcl20fwd": ("qcl_fwd", 20, 6, "complex128",
+                 "config 3: QCL 20 qubits x 6 layers forward losses of a batch of 1024 data points (one circuit each)"),
+    "qcl20b": ("qcl_batch", 20, 6, "complex128",
+               "config 3: QCL 20 qubits x 6 layers full gradients of all 1024 data points (1,474,560 circuits)"),
     "qcl32": ("qcl", 32, 4, "complex64", "config 5: QCL 32 qubits x 4 layers full gradient, complex64"),
     "qcl4": ("qcl", 4, 2, "complex128", "config 1: QCL 4 qubits x 2 layers gradient (one data point)"),
     "mcvqe8": ("mcvqe", 8, 0, "complex128", "config 2: MC-VQE 8-chromophore parameter-shift gradient"),
@@ -249,6 +253,7 @@ def run_reference(args):
     if rank != 0:
         return
     kind, n, layers, precision, desc = WORKLOADS[args.workload]
+    kind = "qcl" if kind.startswith("qcl") else kind   # same circuits, same per-circuit CPU cost
     threads = cpu_threads_for(n) if n > 12 else 1
     for _ in range(args.warmup):
         cpu_sample_rate(kind, n, layers, threads, budget_s=4.0, seed=args.seed)
@@ -274,10 +279,25 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+POINTS = 1024   # config 3's batch of data points
+
+
 def circuits_per_step(kind, n, layers):
     if kind == "mcvqe":
         return 2 * (6 * n - 4) * (5 * n - 4)
+    if kind == "qcl_fwd":
+        return POINTS
+    if kind == "qcl_batch":
+        return POINTS * 12 * n * layers
     return 12 * n * layers
+
+
+class _Step:
+    """Result of one multi-point step: circuits evaluated and a checksum vector."""
+
+    def __init__(self, circuits, values):
+        self.n_circuit_executions = circuits
+        self.gradient = values
 
 
 # ---------------------------------------------------------------------------
@@ -330,6 +350,21 @@ def main():
         spec = qv.DdclSpec(n, layers, theta, target)
         def step():
             return qv.ddcl_gradient(spec, pool, backend_factory=_Factory(device, precision))
+    elif kind in ("qcl_fwd", "qcl_batch"):
+        # data point i: theta seed s+1+i, target seed s+2+i; points
+        # are dealt to ranks round-robin, each rank runs its share on its GPU
+        mine = range(rank, POINTS, world)
+        specs = [qv.DdclSpec(n, layers, qv.random_angles(qv.ddcl_parameter_count(n, layers), s + 1 + i),
+                             qv.random_target_distribution(n, s + 2 + i)) for i in mine]
+        fwd_backend = qv.B200Backend(device=device, precision=precision)
+        one_pool = qv.VqpuPoolConfig(n_virtual_qpus=1)
+
+        def step():
+            if kind == "qcl_fwd":
+                return _Step(POINTS, qv.ddcl_forward_losses(specs, fwd_backend))
+            grads = [qv.ddcl_gradient(sp, one_pool, backend_factory=_Factory(device, precision)).gradient
+                     for sp in specs]
+            return _Step(circuits_per_step(kind, n, layers), np.concatenate(grads))
     else:
         ham = qv.aiem_hamiltonian(qv.random_aiem_coefficients(n, s))
         mspec = qv.McvqeAnsatzSpec(qv.random_cis_amplitudes(n, s + 1), qv.random_angles(qv.mcvqe_parameter_count(n), s + 2))
@@ -351,6 +386,8 @@ def main():
     for _ in range(max(args.warmup, 0)):
         step()
     barrier()
+    keys = ("device_ms", "pass_ms", "pass_bytes", "pass_flops", "launches", "sweeps", "sweeps_unshared",
+            "h2d_bytes", "d2h_bytes")
 
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -361,8 +398,9 @@ def main():
         barrier()
         ev0.record()
         for _ in range(args.steps):
+            before = dict(engine.total_stats)
             rep = step()
-            st = engine.last_stats
+            st = {k: engine.total_stats[k] - before[k] for k in keys}   # every engine call of the step
             dev_ms += st["device_ms"]
             pass_ms += st["pass_ms"]
             pass_bytes += st["pass_bytes"]
@@ -372,7 +410,7 @@ def main():
             unshared += st["sweeps_unshared"]
             h2d += st["h2d_bytes"]
             d2h += st["d2h_bytes"]
-            passes, tile = st["passes_per_circuit"], st["tile_bits"]
+            passes, tile = engine.total_stats["passes_per_circuit"], engine.total_stats["tile_bits"]
             reports.append(rep)
         ev1.record()
         barrier()
@@ -388,7 +426,7 @@ def main():
     else:
         mx = sm = agg
     e2e_ms_max, dev_ms_max = float(mx[0]), float(mx[1])
-    circuits = reports[-1].n_circuit_executions
+    circuits = reports[-1].n_circuit_executions   # whole job (every rank's points)
     steps = args.steps
     value = circuits * steps / (dev_ms_max / 1e3)
     e2e_value = circuits * steps / (e2e_ms_max / 1e3)
@@ -402,7 +440,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads_for(n) if n > 12 else 1
-        rate, sample, impl, used = cpu_sample_rate(kind, n, layers, threads, budget_s=12.0, seed=s)
+        rate, sample, impl, used = cpu_sample_rate("qcl" if kind.startswith("qcl") else kind, n, layers, threads,
+                                                   budget_s=12.0, seed=s)
         cpu = {"value": rate, "unit": UNIT, "cores": used, "kind": impl, "sample": sample}
 
     if rank == 0:
@@ -414,12 +453,16 @@ def main():
             "data": "synthetic (seeded PCG64: theta seed s+1, target seed s+2, reference generators)",
             "config": {
                 "workload": desc, "qubits": n, "layers": layers, "precision": precision,
-                "circuits_per_step": circuits, "step": "one full parameter-shift gradient",
+                "circuits_per_step": circuits,
+                "step": {"qcl_fwd": f"forward JS losses of {POINTS} data points",
+                         "qcl_batch": f"full parameter-shift gradients of {POINTS} data points"}.get(
+                             kind, "one full parameter-shift gradient"),
                 "full_gradient_s": e2e_ms_max / steps / 1e3,
                 "full_gradient_device_s": dev_ms_max / steps / 1e3,
                 "parallelism": f"vqpu{pool.n_virtual_qpus}->gpu{world} (zigzag blocks), NCCL all-gather of losses",
-                "shift_mode": "pair (psi+- = (Psi0 -+ i Xi_k)/sqrt2: one extra state per parameter)"
-                if kind == "qcl" and n > 12 else "direct",
+                "shift_mode": "none (forward pass)" if kind == "qcl_fwd" else
+                "pair (psi+- = (Psi0 -+ i Xi_k)/sqrt2: one extra state per parameter)"
+                if kind.startswith("qcl") and n > 12 else "direct",
                 "passes_per_circuit": passes, "tile_bits": tile,
                 "hbm_sweeps_per_step": float(sm[6]) / steps, "hbm_sweeps_without_prefix_sharing": float(sm[7]) / steps,
                 "l2": "states (2^n x 16 B) far exceed the 126 MB L2; no flush needed",
@@ -432,8 +475,10 @@ def main():
                          "fp64_peak_source": "cuBLAS DGEMM 8192^3 measured in this run" if fp64_peak else None},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / steps,
                     "d2h_bytes_per_step": d2h / steps,
-                    "api": "paper_2406_03466_b200.ddcl_gradient(spec, VqpuPoolConfig, B200Backend)" if kind == "qcl"
-                    else "paper_2406_03466_b200.mcvqe_gradient(...)"},
+                    "api": {"qcl": "paper_2406_03466_b200.ddcl_gradient(spec, VqpuPoolConfig, B200Backend)",
+                            "qcl_fwd": "paper_2406_03466_b200.ddcl_forward_losses(specs, B200Backend)",
+                            "qcl_batch": "paper_2406_03466_b200.ddcl_gradient per data point"}.get(
+                                kind, "paper_2406_03466_b200.mcvqe_gradient(...)")},
             "gpu_launches": int(float(sm[3])),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

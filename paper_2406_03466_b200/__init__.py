@@ -68,6 +68,7 @@ from .qcl import (
     ddcl_circuit,
     ddcl_circuit_template,
     ddcl_distribution,
+    ddcl_forward_losses,
     ddcl_execution_count,
     ddcl_gradient,
     ddcl_parameter_count,
@@ -76,6 +77,7 @@ from .qcl import (
 )
 from .results import ChildResult, ResultBuffer, merge
 from .shift import SHIFT, SHIFT_TAGS, GradientReport, central_difference, shift_table, shifted_batch, shifted_circuits
-from .vqpu import Block, VqpuPoolConfig, consolidate, execute_parallel, execute_values, partition
+from .vqpu import (Block, VqpuPoolConfig, consolidate, execute_parallel, execute_row_values, execute_values,
+                   partition)
 
 __version__ = "0.1.0"

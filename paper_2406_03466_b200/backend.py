@@ -149,6 +149,22 @@ def support_indices(support, n_qubits: int) -> np.ndarray:
     """Sorted unique amplitude indices of a support given as a target
     distribution (bitstring keys), bitstrings, or integer indices."""
     items = list(support.keys()) if isinstance(support, Mapping) else list(support)
+    if items and all(isinstance(item, str) for item in items):
+        # vectorised parse: one uint8 row per bitstring, most significant bit first
+        try:
+            raw = np.frombuffer("".join(items).encode("ascii"), dtype=np.uint8)
+        except UnicodeEncodeError:
+            raw = None
+        if raw is None or raw.size != len(items) * n_qubits or n_qubits > 64:
+            bad = next((it for it in items if len(it) != n_qubits), items[0])
+            raise ValueError(f"bad support bitstring {bad!r} for {n_qubits} qubits")
+        bits = raw.reshape(len(items), n_qubits) - np.uint8(48)
+        if np.any(bits > 1):
+            bad = items[int(np.nonzero(np.any(bits > 1, axis=1))[0][0])]
+            raise ValueError(f"bad support bitstring {bad!r} for {n_qubits} qubits")
+        weights = np.left_shift(np.uint64(1), np.arange(n_qubits - 1, -1, -1, dtype=np.uint64))
+        arr = np.unique((bits.astype(np.uint64) * weights).sum(axis=1, dtype=np.uint64))
+        return arr
     idx = []
     for item in items:
         if isinstance(item, str):
@@ -245,6 +261,17 @@ class B200Backend:
         self.gate_counter += _gate_count(circuits)
         return out
 
+    def support_probabilities(self, circuits: Sequence[Circuit], n_qubits: int, support) -> np.ndarray:
+        """Exact Born probabilities p_c(b) = |<b|psi_c>|^2 / <psi_c|psi_c> of each
+        circuit on the basis states `support` (bit strings or indices, taken in
+        ascending index order; see `support_indices`): float64
+        [len(circuits), len(support)].  Only the support's light cone is swept."""
+        self._check_all(circuits, n_qubits)
+        sup = support_indices(support, n_qubits)
+        flat = self._run(lower_batch(circuits), n_qubits, native.QV_OUT_SUPPORT, circuits, support=sup)
+        self.gate_counter += _gate_count(circuits)
+        return flat.reshape(len(circuits), sup.size + 1)[:, : sup.size]
+
     def shift_js_losses(self, template: Circuit, theta: Sequence[float], target: Mapping[str, float],
                         params: Sequence[int]) -> np.ndarray:
         """JS losses of the circuits with theta[k] + pi/2 and theta[k] - pi/2,
@@ -281,7 +308,7 @@ class B200Backend:
 
     def tile_qubits(self) -> int:
         """Widest register simulated inside one CTA's shared memory."""
-        return 12 if self.precision == "complex128" else 13
+        return 12
 
     # -- internals -----------------------------------------------------------
     def _precheck(self, c, n: int, children: bool = True) -> str:

@@ -627,6 +627,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
     int x = (c + team * G) / nstates;
     int y = (c + team * G) % nstates;
     for (int i = team; c + i * G < items; i += 2) {
+        QV_MARK(0);
         unsigned char* tileb = smem_raw + (size_t)(i % 3) * TILE;
         if (y != cur_y) {
             e = ent[y];
@@ -650,6 +651,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
             }
         }
         team_sync(team);
+        QV_MARK(1);
         // ---- register groups (as pass_kernel) --------------------------------
         if (!zero_tile) {
             const uint32_t boff = (uint32_t)(tileb - smem_raw);
@@ -690,10 +692,12 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
                             if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
                     }
                 }
+                if (g < 29) QV_MARK(2 + 2 * g);
 #pragma unroll
                 for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off[j]) = a[j];
                 if (g + 1 < pd.ng && !sg[g + 1].cta_sync) __syncwarp();
                 else team_sync(team);
+                if (g < 29) QV_MARK(3 + 2 * g);
             }
         }
         // ---- store / reduce: every shared-memory read before the team barrier
@@ -752,6 +756,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
                 acc += norm2(vals[it]);
             }
         }
+        QV_MARK(62);
         team_sync(team);   // the buffer is drained: item i + 3 streams into it
         if (c + (i + 3) * G < items) load_item(next_src, i + 3);
         if (MODE == 1 && store) {

@@ -955,26 +955,41 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     for (int p = 0; p < P; ++p)
         for (int s = plan.pdesc[p].m0; s < plan.pdesc[p].m0 + plan.pdesc[p].nm; ++s) pass_of_slot[s] = p;
 
-    // matrix tables: row 0 = base, row 1 + j = base with the Pauli at gate j
+    // matrix tables: the base circuit's slots, then per shifted gate j only
+    // the matrices of the pass holding it (its chain's first pass), with the
+    // Pauli inserted; every later pass of a chain reads the base table
     std::vector<double> base(slots8);
     circuit_matrices(plan, topo, angles, base.data());
-    std::vector<T> rows((size_t)(nshift + 1) * slots8);
-    for (size_t q = 0; q < slots8; ++q) rows[q] = (T)base[q];
     std::vector<int> start_pass(nshift);
+    std::vector<size_t> mod_off(nshift);
+    size_t mod_len = 0;
     for (int64_t j = 0; j < nshift; ++j) {
         const int64_t g = gates[j];
         if (g < 0 || g >= (int64_t)topo.kind.size() || !is_rotation(topo.kind[g]) || slot_of[g] < 0)
             throw ArgError("gate_index " + std::to_string(g) + " is not a rotation gate of the circuit");
+        start_pass[j] = pass_of_slot[slot_of[g]];
+        mod_off[j] = mod_len;
+        mod_len += (size_t)plan.pdesc[start_pass[j]].nm * 8;
+    }
+    std::vector<T> rows(slots8 + mod_len);
+    for (size_t q = 0; q < slots8; ++q) rows[q] = (T)base[q];
+    for (int64_t j = 0; j < nshift; ++j) {
+        const int64_t g = gates[j];
+        const PassDesc& pd = plan.pdesc[start_pass[j]];
+        T* blk = rows.data() + slots8 + mod_off[j];
+        for (size_t q = 0; q < (size_t)pd.nm * 8; ++q) blk[q] = (T)base[(size_t)pd.m0 * 8 + q];
         double m8[8];
         slot_matrix_with_pauli(plan, topo, angles, slot_of[g], (int32_t)g, m8);
-        T* row = rows.data() + (size_t)(j + 1) * slots8;
-        for (size_t q = 0; q < slots8; ++q) row[q] = (T)base[q];
-        for (int q = 0; q < 8; ++q) row[(size_t)slot_of[g] * 8 + q] = (T)m8[q];
-        start_pass[j] = pass_of_slot[slot_of[g]];
+        for (int q = 0; q < 8; ++q) blk[(size_t)(slot_of[g] - pd.m0) * 8 + q] = (T)m8[q];
     }
     T* d_mats = reinterpret_cast<T*>(E.d_mats.get(rows.size() * sizeof(T)));
     h2d(E, d_mats, rows.data(), rows.size() * sizeof(T));
-    auto mats_of = [&](int64_t row) { return (const void*)(d_mats + (size_t)row * slots8); };
+    auto mats_base = [&]() { return (const void*)d_mats; };
+    // kernels index matrices from the pass's first slot (e.mats + m0): point
+    // the chain's first-pass entry m0 slots before its block (inside d_mats)
+    auto mats_shift = [&](int64_t j) {
+        return (const void*)(d_mats + slots8 + mod_off[j] - (size_t)plan.pdesc[start_pass[j]].m0 * 8);
+    };
 
     EpiArgs ep;
     std::memset(&ep, 0, sizeof(ep));
@@ -1030,7 +1045,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     std::vector<LaunchEntry> ents;
     std::vector<int64_t> slots_tab;
     for (int p = 0; p < P; ++p) {   // phase 1: Psi0
-        ents.push_back({p == 0 ? nullptr : (const void*)psi0, (void*)psi0, mats_of(0), 0, 0, nullptr});
+        ents.push_back({p == 0 ? nullptr : (const void*)psi0, (void*)psi0, mats_base(), 0, 0, nullptr});
         sched.push_back({true, p, ents.size() - 1, 1, F_STORE, frac(p) * ((p ? 1 : 0) + 1)});
     }
     std::vector<std::vector<int64_t>> by_pass(P);
@@ -1047,8 +1062,8 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
                 const size_t off = ents.size();
                 for (int b = 0; b < nb; ++b) {
                     const void* in = pp == p ? (p == 0 ? nullptr : (const void*)trunk) : (const void*)work(b);
-                    ents.push_back({in, lastp ? nullptr : (void*)work(b), mats_of(1 + D[b0 + b]), D[b0 + b], b,
-                                    (const void*)psi0});
+                    ents.push_back({in, lastp ? nullptr : (void*)work(b), pp == p ? mats_shift(D[b0 + b]) : mats_base(),
+                                    D[b0 + b], b, (const void*)psi0});
                 }
                 const double rd = (pp == p && p == 0) ? 0.0 : 1.0;
                 sched.push_back({true, pp, off, nb, lastp ? F_PAIR : F_STORE, nb * frac(pp) * (lastp ? 2.0 : rd + 1.0)});
@@ -1058,7 +1073,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
             sched.push_back({false, 0, off, nb, 0, 0});
         }
         if (p < last_needed) {   // advance the trunk by pass p
-            ents.push_back({p == 0 ? nullptr : (const void*)trunk, (void*)trunk, mats_of(0), 0, 0, nullptr});
+            ents.push_back({p == 0 ? nullptr : (const void*)trunk, (void*)trunk, mats_base(), 0, 0, nullptr});
             sched.push_back({true, p, ents.size() - 1, 1, F_STORE, frac(p) * ((p ? 1 : 0) + 1)});
         }
     }

@@ -116,6 +116,8 @@ class Engine:
         self.device = int(device)
         self.precision = precision
         self.last_stats: dict[str, float] = {}
+        # running sums over every call (per-call values for the two shape stats)
+        self.total_stats: dict[str, float] = dict.fromkeys(STAT_NAMES, 0.0)
 
     def close(self) -> None:
         if self._handle:
@@ -200,6 +202,8 @@ class Engine:
         stats = np.zeros(len(STAT_NAMES), dtype=np.float64)
         self._lib.qv_last_stats(self._handle, stats.ctypes.data, stats.shape[0])
         self.last_stats = dict(zip(STAT_NAMES, stats.tolist()))
+        for k, v in self.last_stats.items():
+            self.total_stats[k] = v if k in ("passes_per_circuit", "tile_bits") else self.total_stats[k] + v
         if code != QV_OK:
             msg = (self._lib.qv_last_error(self._handle) or b"").decode()
             raise NativeError(code, msg, int(self._lib.qv_last_error_circuit(self._handle)))

@@ -170,15 +170,28 @@ def execute_values(circuits: Sequence[Circuit], n_qubits: int, config: VqpuPoolC
     bitwise-identical results.
     """
     _validate_batch(circuits, n_qubits)
+    return execute_row_values(len(circuits), config, backend_factory,
+                              lambda backend, rows: evaluate(backend, [circuits[i] for i in rows]))
+
+
+def execute_row_values(n_rows: int, config: VqpuPoolConfig, backend_factory: Callable[[], Accelerator],
+                       evaluate_rows: Callable) -> tuple[float, np.ndarray]:
+    """`execute_values` over a batch known only by its row count: blocks,
+    ranks and the all-gather are the same, `evaluate_rows(backend, rows)`
+    gets the int64 row indices of its share (ascending).  Used when the batch
+    is a parameter-shift table of one template, so no per-row `Circuit`
+    objects are built (the template was validated when lowered)."""
+    if n_rows < 1:
+        raise ValueError("empty batch")
     if config.mode != "expectation":
         raise ValueError("the scalar fast path evaluates exact (expectation-mode) results")
-    blocks = [b for b in partition(len(circuits), config.n_virtual_qpus) if b.size]
+    blocks = [b for b in partition(n_rows, config.n_virtual_qpus) if b.size]
     dist = _dist_context()
     started = time.perf_counter()
     if dist is None:
         def run_block(block: Block):
             backend = backend_factory()
-            return evaluate(backend, circuits[block.start:block.end])
+            return evaluate_rows(backend, np.arange(block.start, block.end, dtype=np.int64))
         parts = _run_blocks(blocks, run_block)
         values = np.concatenate(parts) if parts else np.zeros(0)
         return time.perf_counter() - started, values
@@ -191,7 +204,7 @@ def execute_values(circuits: Sequence[Circuit], n_qubits: int, config: VqpuPoolC
     local = np.zeros(0, np.float64)
     if mine:
         backend = backend_factory()
-        local = np.asarray(evaluate(backend, [circuits[i] for i in index]), dtype=np.float64)
+        local = np.asarray(evaluate_rows(backend, index.astype(np.int64)), dtype=np.float64)
     per_rank = [sum(b.size for i, b in enumerate(blocks) if owner[i] == r) for r in range(world)]
     width = max(per_rank)
     use_cuda = dist.get_backend() == "nccl"
@@ -202,7 +215,7 @@ def execute_values(circuits: Sequence[Circuit], n_qubits: int, config: VqpuPoolC
     recv = torch.empty(world * width, dtype=torch.float64, device=device)
     dist.all_gather_into_tensor(recv, send)
     gathered = recv.cpu().numpy().reshape(world, width)
-    values = np.empty(len(circuits), np.float64)
+    values = np.empty(n_rows, np.float64)
     for r in range(world):
         owned = [b for i, b in enumerate(blocks) if owner[i] == r]
         cursor = 0

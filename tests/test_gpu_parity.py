@@ -240,3 +240,21 @@ def test_light_cone_untouched_qubits_and_scattered_support(gpu):
             shifted = theta.copy()
             shifted[k] += sign * math.pi / 2
             assert pair[2 * j + s] == pytest.approx(oracle_js(shifted), abs=TOL128), (k, sign)
+
+
+def test_forward_losses_batch_of_points(gpu, golden_large):
+    """Config 3's forward pass: one circuit per data point, each against its
+    own target, in one device batch -- against the reference's JS values and
+    against per-point device losses."""
+    backend = qv.B200Backend(device=0)
+    for case in golden_large["qcl_forward"]:
+        n, layers = case["n"], case["layers"]
+        spec = qv.DdclSpec(n, layers, qv.random_angles(qv.ddcl_parameter_count(n, layers), case["theta_seed"]),
+                           qv.random_target_distribution(n, case["target_seed"]))
+        assert qv.ddcl_forward_losses([spec], backend)[0] == pytest.approx(case["js"], abs=TOL128), n
+    n, layers = 14, 2
+    specs = [qv.DdclSpec(n, layers, qv.random_angles(qv.ddcl_parameter_count(n, layers), 1 + i),
+                         qv.random_target_distribution(n, 2 + i)) for i in range(5)]
+    batch = qv.ddcl_forward_losses(specs, backend)
+    single = [backend.js_losses([qv.ddcl_circuit(s)], n, s.target)[0] for s in specs]
+    assert np.max(np.abs(batch - np.asarray(single))) < 1e-13
