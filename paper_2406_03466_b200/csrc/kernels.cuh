@@ -283,6 +283,18 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         cp_async_wait<0>();   // this item's tile has landed (issued by the previous item)
         __syncthreads();
         QV_MARK(1);
+        // the next item's source, and an L2 prefetch of its tile: one thread
+        // per 128-byte row (the low coalescing bits are thread bits 0..), so
+        // its cp.async at the end of this item hits L2 instead of waiting on HBM
+        const V* next_src = (!DB && w + G < items) ? src_of(xn, yn) : nullptr;
+        if constexpr (MT) {
+            constexpr int ROW = 128 / sizeof(V);
+            if (next_src != nullptr && (tid & (ROW - 1)) == 0) {
+#pragma unroll
+                for (int it = 0; it < NA; ++it)
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(next_src + pd.g_hi[it]));
+            }
+        }
         if (DB && w + G < items) {   // stream the next item's tile in behind this one's math
             issue_from(src_of(xn, yn), smem_raw + ((i & 1) ? 0 : TILE));
             cp_async_commit();
@@ -348,8 +360,6 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         // item's global stores, so its latency overlaps the store phase.
         double acc = 0.0;
         V vals[NA];
-        // the next item's source address, computed while few registers are live
-        const V* next_src = (!DB && w + G < items) ? src_of(xn, yn) : nullptr;
         if (ep.flags & F_SUPPORT) {
             const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
             double* row = ep.sup_out + e.rslot * (ep.S + 1);
