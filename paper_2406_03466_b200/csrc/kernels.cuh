@@ -156,6 +156,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // F_SUPPORT) and defers the global stores behind the next tile's load issue,
 // 2 is the shift-pair epilogue (F_PAIR).  Separate instantiations keep each
 // variant's register footprint to what it uses.
+#ifndef QV_L2_PREFETCH
+#define QV_L2_PREFETCH 0
+#endif
 template <typename T, int TB, bool DB, int MODE>
 #ifndef QV_TB9_MIN_BLOCKS
 #define QV_TB9_MIN_BLOCKS 1
@@ -283,11 +286,12 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
         cp_async_wait<0>();   // this item's tile has landed (issued by the previous item)
         __syncthreads();
         QV_MARK(1);
-        // the next item's source, and an L2 prefetch of its tile: one thread
-        // per 128-byte row (the low coalescing bits are thread bits 0..), so
-        // its cp.async at the end of this item hits L2 instead of waiting on HBM
+        // the next item's source; optionally (QV_L2_PREFETCH) an L2 prefetch of
+        // its tile, one thread per 128-byte row, so its cp.async at the end of
+        // this item would hit L2.  Measured on B200: 2-state launches 7 % faster,
+        // full gradients (38 states per launch) 3 % slower -- off by default.
         const V* next_src = (!DB && w + G < items) ? src_of(xn, yn) : nullptr;
-        if constexpr (MT) {
+        if constexpr (MT && QV_L2_PREFETCH) {
             constexpr int ROW = 128 / sizeof(V);
             if (next_src != nullptr && (tid & (ROW - 1)) == 0) {
 #pragma unroll
