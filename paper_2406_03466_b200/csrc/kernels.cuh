@@ -69,10 +69,20 @@ struct EpiArgs {
 #ifdef QV_TRACE
 // trace[(item * 64 + event) * 16 + warp]: event 0 item start, 1 tile resident,
 // 2 + 2g group g math done, 3 + 2g group g synchronised, 62 store done
+// CTA 0 records warps 0..7 and, for 256-thread CTAs, CTA gridDim/2 (usually
+// its partner on the same SM) records into warp slots 8..15; event 63 = %smid
 #define QV_MARK(ev)                                                                                \
     do {                                                                                           \
-        if (ep.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && i < 8 && (threadIdx.x >> 5) < 16) \
-            ep.trace[((i) * 64 + (ev)) * 16 + (threadIdx.x >> 5)] = clock64();                     \
+        const int qv_slot = (blockIdx.x == 0) ? (int)(threadIdx.x >> 5)                            \
+                            : (blockIdx.x == gridDim.x / 2 && blockDim.x <= 256) ? 8 + (int)(threadIdx.x >> 5) : -1; \
+        if (ep.trace && qv_slot >= 0 && (threadIdx.x & 31) == 0 && i < 8 && qv_slot < 16) {       \
+            long long qv_t;                                                                        \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(qv_t));                              \
+            ep.trace[((i) * 64 + (ev)) * 16 + qv_slot] = qv_t;                                     \
+            unsigned qv_sm;                                                                        \
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(qv_sm));                                     \
+            ep.trace[((i) * 64 + 63) * 16 + qv_slot] = qv_sm;                                      \
+        }                                                                                          \
     } while (0)
 #else
 #define QV_MARK(ev) \
@@ -158,6 +168,19 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // variant's register footprint to what it uses.
 #ifndef QV_L2_PREFETCH
 #define QV_L2_PREFETCH 0
+#endif
+// diagnostic builds only (timing breakdowns; results are wrong)
+#ifndef QV_RING_TOKEN
+#define QV_RING_TOKEN 1
+#endif
+#ifndef QV_STAGGER_NS
+#define QV_STAGGER_NS 0
+#endif
+#ifndef QV_DIAG_NO_MATH
+#define QV_DIAG_NO_MATH 0
+#endif
+#ifndef QV_DIAG_NO_GROUPS
+#define QV_DIAG_NO_GROUPS 0
 #endif
 template <typename T, int TB, bool DB, int MODE>
 #ifndef QV_TB9_MIN_BLOCKS
@@ -248,6 +271,14 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
     auto issue_load = [&](int w, unsigned char* dst) { issue_from(load_src(w), dst); };
     if (blockIdx.x < items) issue_load(blockIdx.x, smem_raw);
     cp_async_commit();
+#if QV_STAGGER_NS
+    // experiment: spread the CTAs' phases (all CTAs otherwise load, compute
+    // and store in lock-step across the whole GPU)
+    if (MT) {
+        const unsigned d = (blockIdx.x % 8) * QV_STAGGER_NS;
+        for (unsigned t = 0; t < d; t += 1000) __nanosleep(1000);
+    }
+#endif
 
     int cur_y = -1;
     LaunchEntry e;
@@ -304,7 +335,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
             cp_async_commit();
         }
         // ---- register groups --------------------------------------------------
-        if (!zero_tile) {
+        if (!zero_tile && !QV_DIAG_NO_GROUPS) {
             // the tile buffer's byte offset (a multiple of 2^16 > every slot
             // offset) is folded into the XOR base: one address op per amplitude
             const uint32_t boff = (uint32_t)(tileb - smem_raw);
@@ -335,7 +366,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
 #pragma unroll
                     for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off[j]);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
+                    for (int r = 0; r < (QV_DIAG_NO_MATH ? 0 : R); ++r) {   // diagnostic builds skip the math
                         const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
                         if (mi >= 0) {
                             if (r > 0) {
@@ -548,6 +579,11 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
 __device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)));
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n"
+                 ::"r"((unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
     unsigned done = 0;
@@ -572,7 +608,8 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
     constexpr size_t TILE = sizeof(V) << K;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + 3 * TILE);              // 3 mbarriers
-    double* sred_all = reinterpret_cast<double*>(full + 4);                          // 2 x 8
+    uint64_t* tok = full + 3;                                                         // 2 compute tokens
+    double* sred_all = reinterpret_cast<double*>(full + 6);                          // 2 x 8
     uint64_t* otab = reinterpret_cast<uint64_t*>(sred_all + 16);                     // 4 x 256 outer offsets
     GroupDesc* sg = reinterpret_cast<GroupDesc*>(otab + 1024);
     V* smat_all = reinterpret_cast<V*>(sg + pd.ng);                                  // 2 x nm x 4
@@ -590,7 +627,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
         const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
         uint4* gdst = reinterpret_cast<uint4*>(sg);
         for (int i = threadIdx.x; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
-        if (threadIdx.x < 3) mbar_init(full + threadIdx.x, 256);
+        if (threadIdx.x < 5) mbar_init(full + threadIdx.x, 256);   // full[0..2], tok[0..1]
         for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
             const int b = idx >> 8, v = idx & 255;
             uint64_t o = 0;
@@ -666,6 +703,17 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
         }
         team_sync(team);
         QV_MARK(1);
+        // Compute token (QV_RING_TOKEN): the teams' register-group phases
+        // alternate A0 B0 A1 B1 ..., so one team computes while the other
+        // stores and its next tile streams in (without it the two teams -- like
+        // every CTA of a plain launch -- fall into lock-step: all compute, then
+        // all stream).  tok[tau] completes when the other team's previous
+        // compute phase ends.
+        const int m_item = i >> 1;   // this team's item counter
+        if (QV_RING_TOKEN) {
+            if (team == 0 && m_item >= 1) mbar_wait(tok + 0, (unsigned)((m_item - 1) & 1));
+            if (team == 1) mbar_wait(tok + 1, (unsigned)(m_item & 1));
+        }
         // ---- register groups (as pass_kernel) --------------------------------
         if (!zero_tile) {
             const uint32_t boff = (uint32_t)(tileb - smem_raw);
@@ -714,6 +762,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
                 if (g < 29) QV_MARK(3 + 2 * g);
             }
         }
+        if (QV_RING_TOKEN) mbar_arrive(tok + (1 - team));   // hand the FP64 pipe to the other team
         // ---- store / reduce: every shared-memory read before the team barrier
         int x3 = x + g3x;   // item i + 3 (loaded by this team for the other one)
         int y3 = y + g3y;

@@ -128,12 +128,15 @@ __global__ void __launch_bounds__(256, 2) micro(double2* out, const double2* mat
     }
 }
 
+static int g_force_per_sm = 0;   // argv[2]: CTAs per SM (0 = occupancy)
+
 template <int V>
 int run(int groups, double2* out, const double2* mats, const Desc* desc, int sms) {
     const size_t smem = 65536 + 8 * sizeof(Desc) + 64 * sizeof(double2);
     CK(cudaFuncSetAttribute(micro<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, micro<V>, 256, smem));
+    if (g_force_per_sm > 0 && g_force_per_sm < per_sm) per_sm = g_force_per_sm;
     const int blocks = per_sm * sms;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -154,6 +157,7 @@ int run(int groups, double2* out, const double2* mats, const Desc* desc, int sms
 
 int main(int argc, char** argv) {
     const int groups = argc > 1 ? atoi(argv[1]) : 4000;
+    g_force_per_sm = argc > 2 ? atoi(argv[2]) : 0;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     double2* out;
