@@ -134,6 +134,13 @@ def _reference_module():
     return qvirt, qb
 
 
+REFERENCE_MAX_QUBITS = 30   # qvirt.backend.MAX_QUBITS (backend.py:31)
+
+
+class NotRunnable(RuntimeError):
+    """The reference cannot run this configuration at all."""
+
+
 def cpu_sample_rate(kind, n, layers, threads, budget_s=12.0, seed=0):
     """Time the reference CPU implementation on a bounded sample of the
     workload, all `threads` host threads busy; returns (evals/s, sample text,
@@ -185,6 +192,9 @@ def cpu_sample_rate(kind, n, layers, threads, budget_s=12.0, seed=0):
         return done / (time.perf_counter() - t0), f"numpy oracle port, {kind} gradients", impl, 1
 
     gates_per_circuit = n + layers * (7 * n - 1)
+    if impl == "reference" and n > REFERENCE_MAX_QUBITS:
+        raise NotRunnable(f"not runnable by the reference: n = {n} > {REFERENCE_MAX_QUBITS} "
+                          "(allocate() guard, backend.py:31)")
     if impl == "reference":
         template = qvirt.ddcl_circuit_template(n, layers)
         theta = qvirt.random_angles(qvirt.ddcl_parameter_count(n, layers), seed + 1)
@@ -255,6 +265,11 @@ def run_reference(args):
     kind, n, layers, precision, desc = WORKLOADS[args.workload]
     kind = "qcl" if kind.startswith("qcl") else kind   # same circuits, same per-circuit CPU cost
     threads = cpu_threads_for(n) if n > 12 else 1
+    if n > REFERENCE_MAX_QUBITS:
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference rejects n = {n} > "
+                          f"{REFERENCE_MAX_QUBITS} qubits (backend.py:31); config 5 is not runnable by it"}),
+              flush=True)
+        return
     for _ in range(args.warmup):
         cpu_sample_rate(kind, n, layers, threads, budget_s=4.0, seed=args.seed)
     rates, samples = [], []
@@ -440,9 +455,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads_for(n) if n > 12 else 1
-        rate, sample, impl, used = cpu_sample_rate("qcl" if kind.startswith("qcl") else kind, n, layers, threads,
-                                                   budget_s=12.0, seed=s)
-        cpu = {"value": rate, "unit": UNIT, "cores": used, "kind": impl, "sample": sample}
+        try:
+            rate, sample, impl, used = cpu_sample_rate("qcl" if kind.startswith("qcl") else kind, n, layers,
+                                                       threads, budget_s=12.0, seed=s)
+            cpu = {"value": rate, "unit": UNIT, "cores": used, "kind": impl, "sample": sample}
+        except NotRunnable as why:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": str(why)}
 
     if rank == 0:
         grad = np.asarray(reports[-1].gradient)
