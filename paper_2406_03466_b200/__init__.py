@@ -75,7 +75,7 @@ from .qcl import (
     js_divergence,
     random_target_distribution,
 )
-from .results import ChildResult, ResultBuffer, merge
+from .results import ChildResult, ResultBuffer, deserialize, dump_buffer, load_buffer, merge, serialize
 from .shift import SHIFT, SHIFT_TAGS, GradientReport, central_difference, shift_table, shifted_batch, shifted_circuits
 from .vqpu import (Block, VqpuPoolConfig, consolidate, execute_parallel, execute_row_values, execute_values,
                    partition)

@@ -611,7 +611,8 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
     uint64_t* tok = full + 3;                                                         // 2 compute tokens
     double* sred_all = reinterpret_cast<double*>(full + 6);                          // 2 x 8
     uint64_t* otab = reinterpret_cast<uint64_t*>(sred_all + 16);                     // 4 x 256 outer offsets
-    GroupDesc* sg = reinterpret_cast<GroupDesc*>(otab + 1024);
+    LaunchEntry* steam = reinterpret_cast<LaunchEntry*>(otab + 1024);                // per-team item entry
+    GroupDesc* sg = reinterpret_cast<GroupDesc*>(steam + 2);
     V* smat_all = reinterpret_cast<V*>(sg + pd.ng);                                  // 2 x nm x 4
     (void)unused;
 
@@ -673,23 +674,22 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
     for (int i = 0; i < 3; ++i)
         if (c + i * G < items && ((i + 1) & 1) == team) load_item(load_src(c + i * G), i);
 
+    // The item's LaunchEntry is uniform across a team: it lives in shared
+    // memory (steam[team]) rather than in every thread's registers, which
+    // keeps the register-group loop free of spills.
     int cur_y = -1;
-    LaunchEntry e;
     int x = (c + team * G) / nstates;
     int y = (c + team * G) % nstates;
     for (int i = team; c + i * G < items; i += 2) {
         QV_MARK(0);
         unsigned char* tileb = smem_raw + (size_t)(i % 3) * TILE;
         if (y != cur_y) {
-            e = ent[y];
-            const V* msrc = reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4;
+            const V* msrc = reinterpret_cast<const V*>(ent[y].mats) + (size_t)pd.m0 * 4;
             for (int q = t; q < pd.nm * 4; q += 256) smat[q] = msrc[q];
+            if (t == 0) steam[team] = ent[y];
             cur_y = y;
         }
-        const bool gen = e.in == nullptr;
-        V* __restrict__ out = reinterpret_cast<V*>(e.out);
-        const bool store = (ep.flags & F_STORE) && out != nullptr;
-        const uint64_t outer = outer_of(x);
+        const bool gen = ent[y].in == nullptr;
         const bool zero_tile = gen && x != 0;
         mbar_wait(full + i % 3, (unsigned)((i / 3) & 1));   // this item's tile has landed
         if (gen) {
@@ -768,6 +768,11 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
         int y3 = y + g3y;
         if (y3 >= nstates) { y3 -= nstates; ++x3; }
         const V* next_src = (c + (i + 3) * G < items) ? src_of(x3, y3) : nullptr;
+        const LaunchEntry& e = steam[team];   // read before the closing team barrier only
+        const uint64_t outer = outer_of(x);
+        V* __restrict__ out = reinterpret_cast<V*>(e.out);
+        const bool store = (ep.flags & F_STORE) && out != nullptr;
+        const int64_t pslot = e.pslot;
         double acc = 0.0;
         V vals[NA];
         if (MODE == 1 && (ep.flags & F_SUPPORT)) {
@@ -794,7 +799,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
             const double B = team_sum(accB, sred, team, t);
             const double C = team_sum(accC, sred, team, t);
             if (t == 0) {
-                double* p = ep.partial + (e.pslot * ntiles + x) * 3;
+                double* p = ep.partial + (pslot * ntiles + x) * 3;
                 p[0] = A;
                 p[1] = B;
                 p[2] = C;
@@ -829,7 +834,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
         }
         if (MODE == 1 && (ep.flags & F_NORM)) {
             const double s = team_sum(acc, sred, team, t);
-            if (t == 0) ep.partial[e.pslot * ntiles + x] = s;
+            if (t == 0) ep.partial[pslot * ntiles + x] = s;
         }
         x += g2x;   // this team's next item, i + 2
         y += g2y;

@@ -328,7 +328,8 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const bool multi = ntiles > 1 && tb == multi_tile_tb<T>();
     const bool ring = multi && use_ring<T>();
     const bool db = multi && !ring && multi_tile_db<T>();
-    const size_t smem = ring ? (sizeof(V) << pd.k) * 3 + 48 + 16 * sizeof(double) + 8192 + (size_t)pd.ng * sizeof(GroupDesc) +
+    const size_t smem = ring ? (sizeof(V) << pd.k) * 3 + 48 + 16 * sizeof(double) + 8192 + 2 * sizeof(LaunchEntry) +
+                                   (size_t)pd.ng * sizeof(GroupDesc) +
                                    (size_t)pd.nm * 8 * sizeof(V)
                              : (sizeof(V) << pd.k) * (db ? 2 : 1) + (size_t)pd.ng * sizeof(GroupDesc) +
                                    (size_t)pd.nm * 4 * sizeof(V) + 32 * sizeof(double) + (multi ? 8192 : 0);

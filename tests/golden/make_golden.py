@@ -171,10 +171,45 @@ def counts_cases():
     return out
 
 
+def buffer_cases():
+    """The reference's text form of result buffers (buffers.py:129-152):
+    exact-mode distributions and expectations, counts, metadata, awkward
+    names and floats, plus the reference's pool output of a small batch."""
+    from qvirt.buffers import ChildResult, serialize
+    cases = []
+    buf = ResultBuffer(n_qubits=3)
+    buf.metadata.update({"vqpu_count": 4, "label": "run 1", "ok": True, "scale": 0.1 + 0.2, "a.b-c_d": -7})
+    buf.append_child(ChildResult(name="k0+", expectation=1.0 / 3.0))
+    buf.append_child(ChildResult(name="with space", expectation=-2.5e-17))
+    buf.append_child(ChildResult(name="c", counts={"101": 5, "000": 2, "011": 1}, shots=8))
+    buf.append_child(ChildResult(name="d", distribution={"111": 0.6, "001": 0.1 + 0.2, "000": 0.1}))
+    cases.append({"text": serialize(buf)})
+    rng = np.random.default_rng(5)
+    batch = []
+    for i in range(4):
+        c = oracles.random_circuit(rng, 3, 12, name=f"p{i}")
+        if i % 2:
+            c = c.with_observable(oracles.random_pauli_term(rng, 3, letters="XZ"))
+        batch.append(c)
+    pool = ResultBuffer(n_qubits=3)
+    qvirt.execute_parallel(pool, batch, VqpuPoolConfig(n_virtual_qpus=2))
+    cases.append({"text": serialize(pool), "n": 3, "n_virtual_qpus": 2,
+                  "batch": [{"gates": gates_json(c), "observable": obs_json(c.observable), "name": c.name}
+                            for c in batch]})
+    counted = ResultBuffer(n_qubits=3)
+    StatevectorBackend().execute(counted, batch, ExecutionConfig(mode="counts", shots=100, seed=3))
+    cases.append({"text": serialize(counted)})
+    return cases
+
+
 def main():
     if "--counts-only" in sys.argv:
         (OUT / "golden_counts.json").write_text(json.dumps(counts_cases()))
         return
+    if "--buffers-only" in sys.argv:
+        (OUT / "golden_buffers.json").write_text(json.dumps(buffer_cases()))
+        return
+    (OUT / "golden_buffers.json").write_text(json.dumps(buffer_cases()))
     t0 = time.time()
     (OUT / "golden_counts.json").write_text(json.dumps(counts_cases()))
     small = {"generator": "tests/golden/make_golden.py", "reference": str(REF),
