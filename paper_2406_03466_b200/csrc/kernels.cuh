@@ -170,6 +170,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #define QV_L2_PREFETCH 0
 #endif
 // diagnostic builds only (timing breakdowns; results are wrong)
+#ifndef QV_RING_SLEEP_NS
+#define QV_RING_SLEEP_NS 200
+#endif
 #ifndef QV_RING_TOKEN
 #define QV_RING_TOKEN 1
 #endif
@@ -584,6 +587,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                  ::"r"((unsigned)__cvta_generic_to_shared(bar))
                  : "memory");
 }
+// waits that may last a whole compute phase back off with __nanosleep so
+// the spinning warps leave the issue slots to the computing team
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (true) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(QV_RING_SLEEP_NS);
+    }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
     unsigned done = 0;
@@ -711,8 +729,8 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
         // compute phase ends.
         const int m_item = i >> 1;   // this team's item counter
         if (QV_RING_TOKEN) {
-            if (team == 0 && m_item >= 1) mbar_wait(tok + 0, (unsigned)((m_item - 1) & 1));
-            if (team == 1) mbar_wait(tok + 1, (unsigned)(m_item & 1));
+            if (team == 0 && m_item >= 1) mbar_wait_sleep(tok + 0, (unsigned)((m_item - 1) & 1));
+            if (team == 1) mbar_wait_sleep(tok + 1, (unsigned)(m_item & 1));
         }
         // ---- register groups (as pass_kernel) --------------------------------
         if (!zero_tile) {
