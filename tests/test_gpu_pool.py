@@ -195,3 +195,40 @@ def test_drop_in_reference_drivers(gpu, golden_small):
                                   qvirt.random_angles(qvirt.mcvqe_parameter_count(4), mc["theta_seed"]))
     mrep = qvirt.mcvqe_gradient(ham, mspec, qvirt.VqpuPoolConfig(n_virtual_qpus=2), backend_factory=qv.B200Backend)
     assert np.max(np.abs(np.array(mrep.gradient) - mc["gradient"])) < 1e-10
+
+
+def test_28_qubit_shift_pairs_against_direct_circuits(gpu):
+    """The benchmark's register size: shift-pair losses (Psi0 -+ i Xi_k on the
+    support's light cone) against direct simulation of the shifted circuits
+    (prefix-shared, every pass full-width for the children path), for the
+    first, a middle and the last parameter."""
+    n, layers = 28, 2
+    theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), 41)
+    target = qv.random_target_distribution(n, 42)
+    spec = qv.DdclSpec(n, layers, theta, target)
+    backend = qv.B200Backend(device=0, support=target)
+    ks = [0, len(theta) // 2, len(theta) - 1]
+    pair = backend.shift_js_losses(qv.ddcl_circuit_template(n, layers), theta, target, ks)
+    batch = qv.ddcl_batch(spec)
+    direct = backend.js_losses([batch[2 * k + s] for k in ks for s in (0, 1)], n, target)
+    assert np.max(np.abs(pair - direct)) < 1e-12
+    buf = qv.ResultBuffer(n_qubits=n)
+    backend.execute(buf, [batch[2 * ks[1]]], qv.ExecutionConfig())
+    assert qv.js_divergence(target, buf.children[0].distribution) == pytest.approx(pair[2], abs=1e-12)
+
+
+def test_28_qubit_light_cone_against_full_width_passes(gpu):
+    """Support probabilities on the 2^10 low indices (light cone: the last
+    passes sweep 1, 4, 1024 tiles; norm taken as 1) against the same support
+    plus index 2^28 - 1, which makes every pass full-width and sweeps the
+    norm: equal to FP64 rounding."""
+    n, layers = 28, 2
+    spec = qv.DdclSpec(n, layers, qv.random_angles(qv.ddcl_parameter_count(n, layers), 43),
+                       qv.random_target_distribution(n, 44))
+    backend = qv.B200Backend(device=0)
+    circ = [qv.ddcl_circuit(spec)]
+    low = np.arange(1 << 10, dtype=np.uint64)
+    narrow = backend.support_probabilities(circ, n, low)
+    wide = backend.support_probabilities(circ, n, np.append(low, np.uint64((1 << n) - 1)))
+    assert np.max(np.abs(narrow[0] - wide[0, : low.size])) < 1e-14
+    assert 0.0 < narrow.sum() < 1.0
