@@ -329,8 +329,14 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
             constexpr int ROW = 128 / sizeof(V);
             if (next_src != nullptr && (tid & (ROW - 1)) == 0) {
 #pragma unroll
-                for (int it = 0; it < NA; ++it)
+                for (int it = 0; it < NA; ++it) {
+#if QV_L2_PREFETCH == 2   // bulk form: the TMA unit moves the 128-byte row into L2
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;\n" ::"l"(next_src + pd.g_hi[it])
+                                 : "memory");
+#else
                     asm volatile("prefetch.global.L2 [%0];\n" ::"l"(next_src + pd.g_hi[it]));
+#endif
+                }
             }
         }
         if (DB && w + G < items) {   // stream the next item's tile in behind this one's math
