@@ -149,6 +149,20 @@ void slot_matrix_with_pauli(const Plan& plan, const Topology& topo, const double
 // Slot holding topology gate g (-1 if g is not a one-qubit gate of the plan).
 std::vector<int> slot_of_gates(const Plan& plan, const Topology& topo);
 
+// Light cone of a support-restricted output (SUPPORT / JS results, shift
+// pairs): per pass, the global bits its tile index ranges over and the local
+// bits it is the first to touch (zero-filled instead of loaded); `reach` =
+// bits any pass touches (support indices outside it have amplitude 0).
+struct LightCone {
+    std::vector<uint64_t> outer_free;
+    std::vector<uint32_t> fresh;
+    uint64_t reach = 0;
+};
+LightCone light_cone(const Plan& plan, const uint64_t* support, int64_t S);
+
+// The pass restricted to the tiles whose outer bits outside `free` are zero.
+PassDesc restrict_pass(const PassDesc& pd, uint64_t free, uint32_t fresh);
+
 #ifdef __CUDACC__
 #define QV_HD __host__ __device__
 #else

@@ -391,60 +391,6 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     E.stats[11] += (double)nstates * amps * 14.0 * pd.nm;
 }
 
-// Light cone of a support-restricted output (SUPPORT / JS results, shift
-// pairs).  Backward: a bit that is zero in every support index and that no
-// pass from p on touches is a spectator -- the final amplitudes on the support
-// only depend on the inputs of pass p whose spectator bits are zero, so
-// cone[p] = support bits | tile bits of passes p..P-1.  Forward: every state
-// starts as |0...0>, so before pass p only the bits some earlier pass touched
-// (seen[p]) can be nonzero.  Pass p then runs on the tiles whose outer bits
-// outside cone[p] & seen[p] are zero, and zero-fills the local slots of bits
-// it is the first to touch (`fresh`) instead of loading them.  For the QCL
-// benchmarks the first two passes touch 1 and 256 tiles and the last three 1,
-// 4 and 1024 tiles of 2^16.  Support indices with a bit no pass touches have
-// probability exactly 0 (`reach` excludes them).
-struct LightCone {
-    std::vector<uint64_t> outer_free;   // per pass: global bits the tile index ranges over
-    std::vector<uint32_t> fresh;        // per pass: logical local bits loaded as zeros
-    uint64_t reach = 0;                 // bits any pass touches
-};
-LightCone light_cone(const Plan& plan, const uint64_t* support, int64_t S) {
-    const size_t P = plan.passes.size();
-    LightCone lc;
-    lc.outer_free.resize(P);
-    lc.fresh.resize(P);
-    uint64_t acc = 0;
-    for (int64_t s = 0; s < S; ++s) acc |= support[s];
-    std::vector<uint64_t> cone(P);
-    for (size_t p = P; p-- > 0;) {
-        for (int b : plan.passes[p].S) acc |= 1ull << b;
-        cone[p] = acc;
-    }
-    uint64_t seen = 0;
-    for (size_t p = 0; p < P; ++p) {
-        lc.outer_free[p] = cone[p] & seen;
-        uint32_t fresh = 0;
-        for (size_t j = 0; j < plan.passes[p].S.size(); ++j)
-            if (!((seen >> plan.passes[p].S[j]) & 1)) fresh |= 1u << j;
-        lc.fresh[p] = fresh;
-        for (int b : plan.passes[p].S) seen |= 1ull << b;
-    }
-    lc.reach = seen;
-    return lc;
-}
-
-// The pass restricted to the tiles whose outer bits outside `free` are zero.
-PassDesc restrict_pass(const PassDesc& pd, uint64_t free, uint32_t fresh) {
-    PassDesc r = pd;
-    int m = 0;
-    for (int j = 0; j < pd.n_outer; ++j)
-        if ((free >> pd.obits[j]) & 1) r.obits[m++] = pd.obits[j];
-    for (int j = m; j < (int)sizeof(r.obits); ++j) r.obits[j] = 0;
-    r.n_outer = m;
-    r.fresh = fresh;
-    return r;
-}
-
 // Support indices bucketed by the tile of the last pass that holds them
 // (CSR over tiles) with their logical local index inside the tile; sets
 // ep.sup_off / sup_local / sup_pos.  Requires ep.S and ep.ntiles.

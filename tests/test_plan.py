@@ -117,3 +117,47 @@ def test_small_register_is_single_tile(plan_lib):
     gates = sv.bind_template(sv.ddcl_template_gates(4, 2), [0.3] * 48)
     st, _ = stats(plan_lib, 4, gates)
     assert st[5] == 1 and st[0] == 1 and st[4] == 4
+
+
+def _simulate_cone(lib, n, gates, tile_bits, support, precision=0):
+    f = lib.qvp_simulate_cone
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_int,
+                                                                            ctypes.c_void_p, ctypes.c_int64,
+                                                                            ctypes.c_void_p, ctypes.c_void_p]
+    kinds, q0, q1, ang = arrays(gates)
+    sup = np.ascontiguousarray(support, dtype=np.uint64)
+    out = np.zeros(sup.size, np.float64)
+    visited = ctypes.c_int64(0)
+    rc = f(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data, ang.ctypes.data, precision, tile_bits,
+           sup.ctypes.data, sup.size, out.ctypes.data, ctypes.byref(visited))
+    assert rc > 0
+    return out, visited.value, rc
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_light_cone_restriction_reads_only_written_data(plan_lib, seed):
+    """The product's light cone (csrc/plan.cpp light_cone / restrict_pass):
+    each pass runs only on the tiles the support can see and zero-fills the
+    slots of bits no earlier pass touched.  The interpreter starts from a
+    NaN-filled state, so reading anything the restricted passes did not
+    write would poison the support probabilities.  Random circuits (some
+    qubits without gates), small tiles (many passes), scattered supports."""
+    rng = np.random.Generator(np.random.PCG64(500 + seed))
+    n = 12 + seed % 3
+    idle = {int(q) for q in rng.choice(n, size=seed % 3, replace=False)}
+    active = [q for q in range(n) if q not in idle]
+    gates = [g for g in sv.random_circuit_gates(rng, n, 90, extended=True) if set(g[1]) <= set(active)]
+    probs = np.abs(sv.run_gates(n, gates)) ** 2
+    tile = (6, 7, 8)[seed % 3]
+    supports = [np.arange(1 << 5, dtype=np.uint64),
+                np.unique(rng.integers(0, 1 << n, 40).astype(np.uint64)),
+                np.array([int(rng.integers(0, 1 << n))], np.uint64),
+                np.array([0, (1 << n) - 1], np.uint64)]
+    for sup in supports:
+        got, visited, passes = _simulate_cone(plan_lib, n, gates, tile, sup)
+        assert not np.any(np.isnan(got)), sup
+        assert np.max(np.abs(got - probs[sup.astype(np.int64)])) < 1e-12, sup
+    # the low-index support sweeps far fewer tiles than the full passes
+    _, visited, passes = _simulate_cone(plan_lib, n, gates, tile, supports[0])
+    assert visited < passes * (1 << (n - tile))
