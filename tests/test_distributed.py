@@ -65,3 +65,44 @@ def test_execute_values_two_ranks(n_circuits, n_vqpus):
         mine = [f"c{i}" for j, b in enumerate(blocks) if qv.vqpu.rank_of_block(j, 2) == rank
                 for i in range(b.start, b.end)]
         assert seen == mine
+
+
+def _row_worker(rank, world, port, n_rows, n_vqpus, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        seen = []
+
+        def evaluate_rows(backend, rows):
+            seen.extend(int(r) for r in rows)
+            return rows * 1.5 + 0.25
+
+        _, values = qv.execute_row_values(n_rows, qv.VqpuPoolConfig(n_virtual_qpus=n_vqpus), StubBackend,
+                                          evaluate_rows)
+        out[rank] = (values.tolist(), seen)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_rows,n_vqpus", [(2688, 16), (9, 4)])
+def test_execute_row_values_two_ranks(n_rows, n_vqpus):
+    """The shift-table path of ddcl_gradient (rows, no Circuit objects): same
+    blocks, zigzag ownership and all-gather as execute_values."""
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_row_worker, args=(2, _free_port(), n_rows, n_vqpus, out), nprocs=2, join=True)
+    want = [i * 1.5 + 0.25 for i in range(n_rows)]
+    blocks = [b for b in qv.partition(n_rows, n_vqpus) if b.size]
+    for rank in range(2):
+        values, seen = out[rank]
+        assert values == want
+        assert seen == [i for j, b in enumerate(blocks) if qv.vqpu.rank_of_block(j, 2) == rank
+                        for i in range(b.start, b.end)]
+
+
+def test_execute_row_values_single_process():
+    _, values = qv.execute_row_values(10, qv.VqpuPoolConfig(n_virtual_qpus=3), StubBackend,
+                                      lambda backend, rows: rows * 2.0)
+    assert values.tolist() == [2.0 * i for i in range(10)]
+    with pytest.raises(ValueError):
+        qv.execute_row_values(0, qv.VqpuPoolConfig(), StubBackend, lambda b, r: r)
