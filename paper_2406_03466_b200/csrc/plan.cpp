@@ -10,6 +10,10 @@
 //   RX = [[c,-is],[-is,c]];  CZ(a,b) = H_b CNOT(a,b) H_b.
 #include "plan.hpp"
 
+#ifndef QV_SWZ_TMA
+#define QV_SWZ_TMA 0
+#endif
+
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -144,7 +148,10 @@ struct GroupBuilder {
 
     uint16_t swz(uint32_t v) const {   // bank swizzle, GF(2)-linear
         uint32_t r = v;
-        for (int j = beta; j < k; ++j)
+        // QV_SWZ_TMA (experiment): fold only bits beta..2*beta-1, the pattern of
+        // TMA's 128-byte swizzle (16-byte chunk ^= row index mod 8)
+        const int top = QV_SWZ_TMA ? std::min(k, 2 * beta) : k;
+        for (int j = beta; j < top; ++j)
             if ((v >> j) & 1u) r ^= 1u << (j % beta);
         return (uint16_t)r;
     }
