@@ -258,3 +258,25 @@ def test_forward_losses_batch_of_points(gpu, golden_large):
     batch = qv.ddcl_forward_losses(specs, backend)
     single = [backend.js_losses([qv.ddcl_circuit(s)], n, s.target)[0] for s in specs]
     assert np.max(np.abs(batch - np.asarray(single))) < 1e-13
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_multi_tile_circuits_fuzz(gpu, seed):
+    """Random circuits on 13-18 qubits (several tiles, all gate kinds incl.
+    the RX / CZ extensions): support probabilities on a scattered support
+    (light-cone passes) and a random Pauli term (full-width passes) against
+    the dense oracle."""
+    rng = np.random.Generator(np.random.PCG64(900 + seed))
+    n = 13 + seed % 6
+    gates = sv.random_circuit_gates(rng, n, 240, extended=True)
+    circ = qv.Circuit(n, tuple(qv.Gate(qv.GateKind(k), t, a) for k, t, a in gates), name="f")
+    amps = sv.run_gates(n, gates)
+    backend = qv.B200Backend(device=0)
+    sup = np.unique(rng.integers(0, 1 << n, 64).astype(np.uint64))
+    got = backend.support_probabilities([circ], n, sup)[0]
+    assert np.max(np.abs(got - np.abs(amps[sup.astype(np.int64)]) ** 2)) < 1e-12
+    letters = rng.choice(list("XYZ"), size=3)
+    qubits = rng.choice(n, size=3, replace=False)
+    term = qv.pauli({int(q): str(p) for q, p in zip(qubits, letters)}, 0.5)
+    want = 0.5 * sv.pauli_expectation(amps, n, *sv.term_masks(term.factors, n))
+    assert backend.expectation_values([circ.with_observable(term)], n)[0] == pytest.approx(want, abs=TOL128)
