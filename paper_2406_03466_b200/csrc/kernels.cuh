@@ -189,12 +189,15 @@ template <typename T, int TB, bool DB, int MODE>
 #ifndef QV_TB9_MIN_BLOCKS
 #define QV_TB9_MIN_BLOCKS 1
 #endif
+#ifndef QV_C128_TB8_MIN_BLOCKS
+#define QV_C128_TB8_MIN_BLOCKS 2   // complex128 at 12 tile bits: two CTAs per SM (128 registers)
+#endif
 #ifndef QV_C64_TB8_MIN_BLOCKS
 #define QV_C64_TB8_MIN_BLOCKS 3   // complex64 at 12 tile bits: three CTAs per SM (<= 85 registers)
 #endif
 __global__ void __launch_bounds__(pass_threads(TB), (DB ? (sizeof(T) == 4 && TB == 8 ? QV_C64_TB8_MIN_BLOCKS : 1)
                                                      : TB >= 9 ? QV_TB9_MIN_BLOCKS
-                                                     : TB == 8 ? (sizeof(T) == 4 ? QV_C64_TB8_MIN_BLOCKS : 2) : 4))
+                                                     : TB == 8 ? (sizeof(T) == 4 ? QV_C64_TB8_MIN_BLOCKS : QV_C128_TB8_MIN_BLOCKS) : 4))
 pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent,
             int nstates, int unused, EpiArgs ep) {
     typedef typename Cx<T>::V V;
