@@ -261,6 +261,18 @@ class B200Backend:
         self.gate_counter += _gate_count(circuits)
         return out
 
+    def pauli_values(self, circuits: Sequence[Circuit], n_qubits: int, term_offsets: np.ndarray,
+                     xmask: np.ndarray, ymask: np.ndarray, zmask: np.ndarray) -> np.ndarray:
+        """Raw <P_t> of Pauli strings given as masks (bit n-1-q for qubit q),
+        terms term_offsets[c]..term_offsets[c+1] on circuit c: float64
+        [term_offsets[-1]].  The circuits' own observables are ignored."""
+        self._check_all(circuits, n_qubits)
+        out = self._run(lower_batch(circuits), n_qubits, native.QV_OUT_PAULI, circuits,
+                        terms=(np.ascontiguousarray(term_offsets, np.int64), np.ascontiguousarray(xmask, np.uint64),
+                               np.ascontiguousarray(ymask, np.uint64), np.ascontiguousarray(zmask, np.uint64)))
+        self.gate_counter += _gate_count(circuits)
+        return out
+
     def support_probabilities(self, circuits: Sequence[Circuit], n_qubits: int, support) -> np.ndarray:
         """Exact Born probabilities p_c(b) = |<b|psi_c>|^2 / <psi_c|psi_c> of each
         circuit on the basis states `support` (bit strings or indices, taken in

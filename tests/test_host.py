@@ -228,3 +228,35 @@ def test_mcvqe_counts_batch_and_wstate():
         assert amps[1 << (4 - k)].real == pytest.approx(a[k], abs=1e-12)
     assert [(g.kind.value, g.targets, g.angle) for g in qv.w_state_prep(a).gates] == \
         [(k, tuple(t), ang) for k, t, ang in sv.w_state_gates(a)]
+
+
+class _OracleRowsBackend:
+    """CPU stand-in exposing `pauli_values` (the B200 fast-path entry point)
+    computed with the numpy oracle: exercises mcvqe_gradient's row
+    bookkeeping (state / term grouping per vQPU block) without a GPU."""
+
+    def __init__(self):
+        self.calls = 0
+
+    def pauli_values(self, circuits, n, offsets, xm, ym, zm):
+        self.calls += 1
+        out = []
+        for i, c in enumerate(circuits):
+            amps = sv.run_gates(n, [(g.kind.value, g.targets, g.angle) for g in c.gates])
+            for j in range(int(offsets[i]), int(offsets[i + 1])):
+                ny = bin(int(ym[j])).count("1")
+                out.append(sv.pauli_expectation(amps, n, int(xm[j]), int(ym[j]), int(zm[j]), ny))
+        return np.asarray(out)
+
+
+@pytest.mark.parametrize("n_vqpus", [1, 5, 17])
+def test_mcvqe_row_fast_path_matches_reference(golden_small, n_vqpus):
+    case = golden_small["mcvqe"][2]   # 3 monomers
+    n = case["n"]
+    ham = qv.aiem_hamiltonian(qv.random_aiem_coefficients(n, case["coeff_seed"]))
+    spec = qv.McvqeAnsatzSpec(qv.random_cis_amplitudes(n, case["cis_seed"]),
+                              qv.random_angles(qv.mcvqe_parameter_count(n), case["theta_seed"]))
+    backend = _OracleRowsBackend()
+    rep = qv.mcvqe_gradient(ham, spec, qv.VqpuPoolConfig(n_virtual_qpus=n_vqpus), backend_factory=lambda: backend)
+    assert rep.n_circuit_executions == case["n_circuits"]
+    assert np.max(np.abs(np.asarray(rep.gradient) - case["gradient"])) < 1e-10
