@@ -27,7 +27,7 @@ import itertools
 import math
 import threading
 from dataclasses import dataclass
-from typing import Iterable, Mapping, Protocol, Sequence
+from typing import Callable, Iterable, Mapping, Protocol, Sequence
 
 import numpy as np
 
@@ -283,6 +283,33 @@ class B200Backend:
         flat = self._run(lower_batch(circuits), n_qubits, native.QV_OUT_SUPPORT, circuits, support=sup)
         self.gate_counter += _gate_count(circuits)
         return flat.reshape(len(circuits), sup.size + 1)[:, : sup.size]
+
+    def js_losses_rows(self, template: Circuit, values: np.ndarray, target: Mapping[str, float],
+                       name_of: Callable[[int], str] | None = None) -> np.ndarray:
+        """`js_losses` of the template bound to each parameter row of `values`
+        ([rows, n_params]): one uniform lowered batch, no per-row circuit
+        objects (the parameter-shift tables of the gradient drivers)."""
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        lw = template.lowering()
+        if values.ndim != 2 or values.shape[1] != lw.n_params:
+            raise ValueError(f"expected rows of {lw.n_params} parameter values")
+        if not np.all(np.isfinite(values)):
+            raise ValueError("non-finite angle")
+        n = template.n_qubits
+        lowered = native.LoweredBatch(values.shape[0], True, lw.kinds.shape[0], None, lw.kinds, lw.q0, lw.q1,
+                                      lw.gate_angles(values))
+        keys = sorted(target)
+        sup = support_indices(keys, n)
+        order = np.argsort(np.asarray([int(k, 2) for k in keys], dtype=np.uint64), kind="stable")
+        p = np.asarray([float(target[k]) for k in keys], dtype=np.float64)[order]
+        try:
+            out = self._engine.execute(n, lowered, native.QV_OUT_JS, support=sup, target=p)
+        except native.NativeError as err:
+            name = name_of(err.circuit) if name_of else f"{template.name}[row {err.circuit}]"
+            raise ExecutionError(name, str(err)) from err
+        self.last_stats = dict(self._engine.last_stats)
+        self.gate_counter += values.shape[0] * int(lw.kinds.shape[0])
+        return out
 
     def shift_js_losses(self, template: Circuit, theta: Sequence[float], target: Mapping[str, float],
                         params: Sequence[int]) -> np.ndarray:
