@@ -107,6 +107,26 @@ struct Engine {
     DevBuf<int32_t> d_sup_off, d_sup_local, d_sup_pos;
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
+    // pinned staging for host->device copies: a call's inputs are copied into
+    // it and sent with truly asynchronous cudaMemcpyAsync (pageable sources
+    // would each be staged synchronously by the driver).  Reset per call;
+    // every call ends with a stream synchronisation.
+    unsigned char* pinned = nullptr;
+    size_t pinned_cap = 0, pinned_used = 0;
+
+    unsigned char* stage(size_t bytes) {
+        const size_t need = (bytes + 255) & ~(size_t)255;
+        if (pinned_used + need > pinned_cap) {
+            CK(cudaStreamSynchronize(stream));   // pending copies may still read the old buffer
+            if (pinned) CK(cudaFreeHost(pinned));
+            pinned_cap = std::max<size_t>({need, 2 * pinned_cap, (size_t)1 << 20});
+            CK(cudaMallocHost(reinterpret_cast<void**>(&pinned), pinned_cap));
+            pinned_used = 0;
+        }
+        unsigned char* at = pinned + pinned_used;
+        pinned_used += need;
+        return at;
+    }
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;   // pass-kernel (start, stop) of this call
 
     size_t amp_bytes() const { return precision == 0 ? 16 : 8; }
@@ -124,7 +144,10 @@ struct Engine {
 
 // Host<->device copies of a call, counted for the e2e byte figures (stats[9], [10]).
 inline void h2d(Engine& E, void* dst, const void* src, size_t bytes) {
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, E.stream));
+    if (bytes == 0) return;
+    unsigned char* staged = E.stage(bytes);
+    std::memcpy(staged, src, bytes);
+    CK(cudaMemcpyAsync(dst, staged, bytes, cudaMemcpyHostToDevice, E.stream));
     E.stats[9] += (double)bytes;
 }
 inline void d2h(Engine& E, void* dst, const void* src, size_t bytes) {
@@ -826,6 +849,8 @@ void execute(Engine& E, const qv_circuits* c, const qv_results* r, double* out, 
     CK(cudaSetDevice(E.device));
     std::memset(E.stats, 0, sizeof(E.stats));
     E.events_used = 0;
+    CK(cudaStreamSynchronize(E.stream));   // an earlier failed call may have copies in flight
+    E.pinned_used = 0;
     E.timed.clear();
     const int n = c->n_qubits;
 
@@ -1067,6 +1092,8 @@ void shift_js(Engine& E, const qv_circuits* c, int64_t nshift, const int64_t* ga
     CK(cudaSetDevice(E.device));
     std::memset(E.stats, 0, sizeof(E.stats));
     E.events_used = 0;
+    CK(cudaStreamSynchronize(E.stream));   // an earlier failed call may have copies in flight
+    E.pinned_used = 0;
     E.timed.clear();
     Topology t;
     t.n = c->n_qubits;
@@ -1146,6 +1173,8 @@ int qv_destroy(qv_handle h) {
         E->d_pauli_out.release(); E->d_target.release(); E->d_support.release(); E->d_tflip.release();
         E->d_tphase.release(); E->d_term_off.release(); E->d_slots.release(); E->d_sup_off.release();
         E->d_sup_local.release(); E->d_sup_pos.release();
+        if (E->pinned) cudaFreeHost(E->pinned);
+        E->pinned = nullptr;
         for (auto& kv : E->plans) kv.second->d_groups.release();
         for (auto e : E->events) cudaEventDestroy(e);
         if (E->stream) cudaStreamDestroy(E->stream);
