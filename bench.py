@@ -47,6 +47,9 @@ WORKLOADS = {
                "config 3: QCL 20 qubits x 6 layers full gradients of all 1024 data points (1,474,560 circuits)"),
     "qcl32": ("qcl", 32, 4, "complex64", "config 5: QCL 32 qubits x 4 layers full gradient, complex64"),
     "qcl4": ("qcl", 4, 2, "complex128", "config 1: QCL 4 qubits x 2 layers gradient (one data point)"),
+    # the paper's own DDCL strong-scaling workloads (Table 2/3: L = 10)
+    "ddcl20l10": ("qcl", 20, 10, "complex128", "paper Table 3: DDCL 20 qubits x 10 layers full gradient (2400 circuits)"),
+    "ddcl26l10": ("qcl", 26, 10, "complex128", "paper Table 3: DDCL 26 qubits x 10 layers full gradient (3120 circuits)"),
     "mcvqe8": ("mcvqe", 8, 0, "complex128", "config 2: MC-VQE 8-chromophore parameter-shift gradient"),
 }
 
@@ -296,6 +299,21 @@ def run_reference(args):
 
 POINTS = 1024   # config 3's batch of data points
 
+# the paper's published strong-scaling fits (Table 3,
+# PAPER.md:303-325), log10(seconds) = a * log2(GPUs) + b, V100 + cuStateVec,
+# sampled counts mode -- the only published numbers for this path.
+PAPER_FITS = {(20, 10): (-0.132, 2.622), (22, 10): (-0.137, 2.726), (24, 10): (-0.159, 2.958),
+              (26, 10): (-0.204, 3.398)}
+
+
+def paper_rate(n, layers, gpus):
+    """Circuit evals/s of the paper's fit at this GPU count, or None."""
+    fit = PAPER_FITS.get((n, layers))
+    if fit is None:
+        return None
+    seconds = 10 ** (fit[0] * math.log2(gpus) + fit[1])
+    return 12 * n * layers / seconds
+
 
 def circuits_per_step(kind, n, layers):
     if kind == "mcvqe":
@@ -466,7 +484,9 @@ def main():
         grad = np.asarray(reports[-1].gradient)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": dev_ms_max / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": dev_ms_max / steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": (value / paper_rate(n, layers, world)) if (kind == "qcl" and paper_rate(n, layers, world))
+            else None,
             "dtype": "c128 (f64)" if precision == "complex128" else "c64 (f32, f64 reductions)",
             "data": "synthetic (seeded PCG64: theta seed s+1, target seed s+2, reference generators)",
             "config": {
@@ -485,6 +505,9 @@ def main():
                 "hbm_sweeps_per_step": float(sm[6]) / steps, "hbm_sweeps_without_prefix_sharing": float(sm[7]) / steps,
                 "l2": "states (2^n x 16 B) far exceed the 126 MB L2; no flush needed",
                 "gradient_checksum": float(np.sum(grad)), "seed": s,
+                **({"vs_baseline_source": "paper Table 3 fit at this GPU count (V100 + cuStateVec, sampled "
+                                          "counts mode; BASELINE.md section 1); this run is exact mode"}
+                   if kind == "qcl" and paper_rate(n, layers, world) else {}),
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak if hbm_peak else None, **_ncu_traffic(),
