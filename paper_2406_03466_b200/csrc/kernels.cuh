@@ -176,9 +176,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef QV_RING_TOKEN
 #define QV_RING_TOKEN 1
 #endif
-#ifndef QV_STAGGER_NS
-#define QV_STAGGER_NS 0
-#endif
 #ifndef QV_DIAG_NO_MATH
 #define QV_DIAG_NO_MATH 0
 #endif
@@ -277,14 +274,6 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
     auto issue_load = [&](int w, unsigned char* dst) { issue_from(load_src(w), dst); };
     if (blockIdx.x < items) issue_load(blockIdx.x, smem_raw);
     cp_async_commit();
-#if QV_STAGGER_NS
-    // experiment: spread the CTAs' phases (all CTAs otherwise load, compute
-    // and store in lock-step across the whole GPU)
-    if (MT) {
-        const unsigned d = (blockIdx.x % 8) * QV_STAGGER_NS;
-        for (unsigned t = 0; t < d; t += 1000) __nanosleep(1000);
-    }
-#endif
 
     int cur_y = -1;
     LaunchEntry e;
