@@ -363,6 +363,10 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     // persistent CTAs: enough per state to fill every SM at full occupancy
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+    // QVB200_CTAS_PER_SM caps the persistent grid (experiments with several
+    // engines sharing one GPU)
+    static const int cap = getenv("QVB200_CTAS_PER_SM") ? atoi(getenv("QVB200_CTAS_PER_SM")) : 0;
+    if (cap > 0) per_sm = std::min(per_sm, cap);
     per_sm = std::max(per_sm, 1);
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E.device));
