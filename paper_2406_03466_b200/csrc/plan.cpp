@@ -296,111 +296,166 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
     } else {
         plan.passes = select_passes(n, k, coalesce_bits(precision), plan.ops);
     }
-    for (auto& pp : plan.passes) {
-        PassDesc d;
-        std::memset(&d, 0, sizeof(d));
-        d.k = k;
-        d.n_outer = plan.single_tile ? 0 : n - k;
-        int logical_of[64];
-        for (int b = 0; b < 64; ++b) logical_of[b] = -1;
-        for (int j = 0; j < k; ++j) { d.sbits[j] = (uint8_t)pp.S[j]; logical_of[pp.S[j]] = j; }
-        if (!plan.single_tile) {
-            int o = 0;
-            for (int b = 0; b < n; ++b)
-                if (logical_of[b] < 0) d.obits[o++] = (uint8_t)b;
-        }
-        const int R = reg_bits(precision);
-        GroupBuilder gb;
-        gb.k = k;
-        gb.beta = beta;
-        gb.rbits = R;
-        gb.amp_shift = precision == 0 ? 4 : 3;
-        for (int j = 0; j < 16; ++j) gb.col[j] = (uint16_t)(j < k ? 1u << j : 0);
-        for (int j = 0; j < k; ++j) d.swz[j] = gb.phys(j);
-        d.g0 = (int)plan.groups.size();
-        d.m0 = (int)plan.mat_op.size();
-        int local_mats = 0;
-        // List scheduling of the pass's op DAG (edges: program order on shared
-        // bits).  Ready CNOTs are folded into Q immediately (free); register
-        // groups are filled with up to R ready MAT1s, longest remaining
-        // dependency chain first, so groups are full and few.
-        const int m = (int)pp.ops.size();
-        std::vector<std::vector<int>> preds(m), succs(m);
-        {
-            std::vector<int> last(64, -1);
-            for (int i = 0; i < m; ++i) {
-                const FusedOp& op = plan.ops[pp.ops[i]];
-                const int bits[2] = {op.b0, op.cnot ? op.b1 : -1};
-                for (int b : bits) {
-                    if (b < 0) continue;
-                    if (last[b] >= 0) { preds[i].push_back(last[b]); succs[last[b]].push_back(i); }
-                    last[b] = i;
+    // Bank model of one pass's groups (warp 0; the other warps differ by a
+    // constant XOR): wavefronts of its loads + stores, 128-bit (complex128)
+    // or 64-bit (complex64) accesses.
+    auto bank_wavefronts = [&](const PassDesc& d) {
+        const int sh = precision == 0 ? 4 : 3, rows = precision == 0 ? 8 : 16;
+        int64_t wf = 0;
+        for (int g = d.g0; g < d.g0 + d.ng; ++g) {
+            const GroupDesc& G = plan.groups[g];
+            for (int j = 0; j < (1 << reg_bits(precision)); ++j) {
+                int count[16] = {0};
+                for (int lane = 0; lane < 32; ++lane) {
+                    uint32_t base = 0;
+                    for (int m = 0; m < 5 && m < k - reg_bits(precision); ++m)
+                        if ((lane >> m) & 1) base ^= G.tcol[m];
+                    ++count[((base ^ G.combo[j]) >> sh) & (rows - 1)];
                 }
+                wf += 2 * *std::max_element(count, count + rows);
             }
         }
-        std::vector<int> height(m, 0);
-        for (int i = m - 1; i >= 0; --i)
-            for (int s : succs[i]) height[i] = std::max(height[i], height[s] + 1);
-        std::vector<char> applied(m, 0), in_group(m, 0);
-        std::vector<int> open_ops;
-        int done = 0;
-        auto ready = [&](int i) {
-            for (int p : preds[i])
-                if (!applied[p]) return false;
-            return true;
-        };
-        auto close_group = [&]() {
-            gb.close();
-            for (int i : open_ops) { applied[i] = 1; ++done; }
-            open_ops.clear();
-        };
-        while (done < m) {
-            bool progress = true;
-            while (progress) {   // fold every ready CNOT into the slot map
-                progress = false;
+        return wf;
+    };
+    for (auto& pp : plan.passes) {
+        auto build_pass = [&](const uint16_t* init_cols) {
+            PassDesc d;
+            std::memset(&d, 0, sizeof(d));
+            d.k = k;
+            d.n_outer = plan.single_tile ? 0 : n - k;
+            int logical_of[64];
+            for (int b = 0; b < 64; ++b) logical_of[b] = -1;
+            for (int j = 0; j < k; ++j) { d.sbits[j] = (uint8_t)pp.S[j]; logical_of[pp.S[j]] = j; }
+            if (!plan.single_tile) {
+                int o = 0;
+                for (int b = 0; b < n; ++b)
+                    if (logical_of[b] < 0) d.obits[o++] = (uint8_t)b;
+            }
+            const int R = reg_bits(precision);
+            GroupBuilder gb;
+            gb.k = k;
+            gb.beta = beta;
+            gb.rbits = R;
+            gb.amp_shift = precision == 0 ? 4 : 3;
+            for (int j = 0; j < 16; ++j) gb.col[j] = init_cols[j];
+            for (int j = 0; j < k; ++j) d.swz[j] = gb.phys(j);
+            d.g0 = (int)plan.groups.size();
+            d.m0 = (int)plan.mat_op.size();
+            int local_mats = 0;
+            // List scheduling of the pass's op DAG (edges: program order on shared
+            // bits).  Ready CNOTs are folded into Q immediately (free); register
+            // groups are filled with up to R ready MAT1s, longest remaining
+            // dependency chain first, so groups are full and few.
+            const int m = (int)pp.ops.size();
+            std::vector<std::vector<int>> preds(m), succs(m);
+            {
+                std::vector<int> last(64, -1);
                 for (int i = 0; i < m; ++i) {
                     const FusedOp& op = plan.ops[pp.ops[i]];
-                    if (!op.cnot || applied[i] || !ready(i)) continue;
-                    gb.cnot(logical_of[op.b0], logical_of[op.b1]);
-                    applied[i] = 1;
-                    ++done;
-                    progress = true;
+                    const int bits[2] = {op.b0, op.cnot ? op.b1 : -1};
+                    for (int b : bits) {
+                        if (b < 0) continue;
+                        if (last[b] >= 0) { preds[i].push_back(last[b]); succs[last[b]].push_back(i); }
+                        last[b] = i;
+                    }
                 }
             }
-            if (done == m) break;
-            int best = -1;
-            for (int i = 0; i < m; ++i) {
-                if (plan.ops[pp.ops[i]].cnot || applied[i] || in_group[i] || !ready(i)) continue;
-                if (best < 0 || height[i] > height[best]) best = i;
+            std::vector<int> height(m, 0);
+            for (int i = m - 1; i >= 0; --i)
+                for (int s : succs[i]) height[i] = std::max(height[i], height[s] + 1);
+            std::vector<char> applied(m, 0), in_group(m, 0);
+            std::vector<int> open_ops;
+            int done = 0;
+            auto ready = [&](int i) {
+                for (int p : preds[i])
+                    if (!applied[p]) return false;
+                return true;
+            };
+            auto close_group = [&]() {
+                gb.close();
+                for (int i : open_ops) { applied[i] = 1; ++done; }
+                open_ops.clear();
+            };
+            while (done < m) {
+                bool progress = true;
+                while (progress) {   // fold every ready CNOT into the slot map
+                    progress = false;
+                    for (int i = 0; i < m; ++i) {
+                        const FusedOp& op = plan.ops[pp.ops[i]];
+                        if (!op.cnot || applied[i] || !ready(i)) continue;
+                        gb.cnot(logical_of[op.b0], logical_of[op.b1]);
+                        applied[i] = 1;
+                        ++done;
+                        progress = true;
+                    }
+                }
+                if (done == m) break;
+                int best = -1;
+                for (int i = 0; i < m; ++i) {
+                    if (plan.ops[pp.ops[i]].cnot || applied[i] || in_group[i] || !ready(i)) continue;
+                    if (best < 0 || height[i] > height[best]) best = i;
+                }
+                if (best < 0) {
+                    if (open_ops.empty()) throw std::runtime_error("group scheduler stalled");
+                    close_group();
+                    continue;
+                }
+                in_group[best] = 1;
+                open_ops.push_back(best);
+                gb.open.push_back({logical_of[plan.ops[pp.ops[best]].b0], local_mats++});
+                plan.mat_op.push_back(pp.ops[best]);
+                if ((int)open_ops.size() == R) close_group();
             }
-            if (best < 0) {
-                if (open_ops.empty()) throw std::runtime_error("group scheduler stalled");
-                close_group();
-                continue;
+            close_group();
+            gb.emit(plan.groups);
+            d.ng = (int)plan.groups.size() - d.g0;
+            d.nm = local_mats;
+            for (int j = 0; j < k; ++j) d.fin[j] = gb.phys(j);
+            for (int it = 0; it < (1 << R); ++it) {   // a thread's amplitudes: tid | it << (k - R)
+                const uint32_t idx = (uint32_t)it << (k - R);
+                d.swz_hi[it] = (uint16_t)apply_cols(d.swz, k, idx);
+                d.fin_hi[it] = (uint16_t)apply_cols(d.fin, k, idx);
+                uint64_t g = 0;
+                for (int i = 0; i < R; ++i)
+                    if ((it >> i) & 1) g |= 1ull << d.sbits[k - R + i];
+                d.g_hi[it] = g;
             }
-            in_group[best] = 1;
-            open_ops.push_back(best);
-            gb.open.push_back({logical_of[plan.ops[pp.ops[best]].b0], local_mats++});
-            plan.mat_op.push_back(pp.ops[best]);
-            if ((int)open_ops.size() == R) close_group();
+            pp.n_groups = d.ng;
+            pp.n_mats = d.nm;
+            plan.pdesc.push_back(d);
+            };
+        uint16_t ident[16];
+        for (int j = 0; j < 16; ++j) ident[j] = (uint16_t)(j < k ? 1u << j : 0);
+        if (!QV_SWZ_TMA || plan.single_tile || beta != 3 || k < 2 * beta + 1) {   // complex128 rows only
+            build_pass(ident);
+            continue;
         }
-        close_group();
-        gb.emit(plan.groups);
-        d.ng = (int)plan.groups.size() - d.g0;
-        d.nm = local_mats;
-        for (int j = 0; j < k; ++j) d.fin[j] = gb.phys(j);
-        for (int it = 0; it < (1 << R); ++it) {   // a thread's amplitudes: tid | it << (k - R)
-            const uint32_t idx = (uint32_t)it << (k - R);
-            d.swz_hi[it] = (uint16_t)apply_cols(d.swz, k, idx);
-            d.fin_hi[it] = (uint16_t)apply_cols(d.fin, k, idx);
-            uint64_t g = 0;
-            for (int i = 0; i < R; ++i)
-                if ((it >> i) & 1) g |= 1ull << d.sbits[k - R + i];
-            d.g_hi[it] = g;
-        }
-        pp.n_groups = d.ng;
-        pp.n_mats = d.nm;
-        plan.pdesc.push_back(d);
+        // QV_SWZ_TMA: the tile bits at physical positions beta..2*beta-1 are
+        // the ones the 128-byte TMA swizzle folds into the bank bits; try every
+        // choice of them and keep the layout with the fewest bank wavefronts
+        uint16_t best[16];
+        int64_t best_wf = -1;
+        for (int a = beta; a < k; ++a)
+            for (int b = a + 1; b < k; ++b)
+                for (int c = b + 1; c < k; ++c) {
+                    uint16_t cols[16] = {0};
+                    int next = 2 * beta;
+                    for (int j = 0; j < k; ++j) {
+                        int pos = j < beta ? j : j == a ? beta : j == b ? beta + 1 : j == c ? beta + 2 : next++;
+                        cols[j] = (uint16_t)(1u << pos);
+                    }
+                    const size_t g0 = plan.groups.size(), m0 = plan.mat_op.size(), p0 = plan.pdesc.size();
+                    build_pass(cols);
+                    const int64_t wf = bank_wavefronts(plan.pdesc.back());
+                    plan.groups.resize(g0);
+                    plan.mat_op.resize(m0);
+                    plan.pdesc.resize(p0);
+                    if (best_wf < 0 || wf < best_wf) {
+                        best_wf = wf;
+                        std::memcpy(best, cols, sizeof(best));
+                    }
+                }
+        build_pass(best);
     }
     return plan;
 }
