@@ -100,7 +100,12 @@ typedef struct qv_results {
     const uint64_t* zmask;
     /* QV_OUT_SUPPORT / QV_OUT_JS: one support shared by the whole batch,
      * sorted ascending, unique amplitude indices; `target` (JS only) holds the
-     * target probability of each support index.                                */
+     * target probability of each support index.  These results are computed
+     * on the support's light cone: a pass only sweeps the tiles the support
+     * can see.  When the last pass is restricted that way the state norm is
+     * not swept and is taken as 1 (the circuits are unitary; the reference's
+     * normalising sum differs from 1 by ~1e-15), so the SUPPORT row's norm
+     * entry then reads exactly 1.                                             */
     int64_t support_count;
     const uint64_t* support;
     const double* target;
