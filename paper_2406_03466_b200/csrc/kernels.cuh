@@ -94,12 +94,14 @@ template <typename T> struct Cx;
 template <> struct Cx<double> { typedef double2 V; };
 template <> struct Cx<float> { typedef float2 V; };
 
-// (u, v) <- [[m00, m01], [m10, m11]] (u, v); 4 multiplies + 12 FMAs per pair.
+// (u, v) <- [[m00, m01], [m10, m11]] (u, v) with m00 REAL (the host removes
+// each fused matrix's global phase, normalise_phase in qvb200.cu): 4
+// multiplies + 10 FMAs per pair instead of 4 + 12.
 template <typename V>
 __device__ __forceinline__ void rot2(const V m00, const V m01, const V m10, const V m11, V& u, V& v) {
     V a, b;
-    a.x = fma(m00.x, u.x, fma(-m00.y, u.y, fma(m01.x, v.x, -m01.y * v.y)));
-    a.y = fma(m00.x, u.y, fma(m00.y, u.x, fma(m01.x, v.y, m01.y * v.x)));
+    a.x = fma(m00.x, u.x, fma(m01.x, v.x, -m01.y * v.y));
+    a.y = fma(m00.x, u.y, fma(m01.x, v.y, m01.y * v.x));
     b.x = fma(m10.x, u.x, fma(-m10.y, u.y, fma(m11.x, v.x, -m11.y * v.y)));
     b.y = fma(m10.x, u.y, fma(m10.y, u.x, fma(m11.x, v.y, m11.y * v.x)));
     u = a;
@@ -410,7 +412,7 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
             // support index the same three terms (finalize_pair_kernel forms
             // p(t +- pi/2) = |Psi0 -+ i Xi|^2 / 2 from them).
             const V* __restrict__ aux = reinterpret_cast<const V*>(e.aux);
-            double accB = 0.0, accC = 0.0;
+            double accB = 0.0, accC = 0.0, accD = 0.0;
             if (active) {
                 const V* __restrict__ src = aux + (outer | tg);
 #pragma unroll
@@ -419,17 +421,20 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
                     const V u = __ldcs(src + pd.g_hi[it]);
                     acc += norm2(u);
                     accB += norm2(v);
-                    accC += (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+                    accC += (double)u.y * (double)v.x - (double)u.x * (double)v.y;   // Im(u conj v)
+                    accD += (double)u.x * (double)v.x + (double)u.y * (double)v.y;   // Re(u conj v)
                 }
             }
             const double A = block_sum(acc, sred);
             const double B = block_sum(accB, sred);
             const double C = block_sum(accC, sred);
+            const double D = block_sum(accD, sred);
             if (tid == 0) {
-                double* p = ep.partial + (e.pslot * ntiles + x) * 3;
+                double* p = ep.partial + (e.pslot * ntiles + x) * 4;
                 p[0] = A;
                 p[1] = B;
                 p[2] = C;
+                p[3] = D;
             }
             const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
             for (int32_t q = lo + tid; q < hi; q += blockDim.x) {
@@ -439,10 +444,11 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
                 for (int j = 0; j < K; ++j)
                     if ((loc >> j) & 1u) gidx |= 1ull << pd.sbits[j];
                 const V u = aux[gidx];
-                double* row = ep.pair_sup + (e.rslot * ep.S + ep.sup_pos[q]) * 3;
+                double* row = ep.pair_sup + (e.rslot * ep.S + ep.sup_pos[q]) * 4;
                 row[0] = norm2(u);
                 row[1] = norm2(v);
                 row[2] = (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+                row[3] = (double)u.x * (double)v.x + (double)u.y * (double)v.y;
             }
         } else if (PLAIN && active) {
 #pragma unroll
@@ -801,7 +807,7 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
         }
         if (MODE == 2) {
             const V* __restrict__ aux = reinterpret_cast<const V*>(e.aux);
-            double accB = 0.0, accC = 0.0;
+            double accB = 0.0, accC = 0.0, accD = 0.0;
             const V* __restrict__ src = aux + (outer | tg);
 #pragma unroll
             for (int it = 0; it < NA; ++it) {
@@ -810,15 +816,18 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
                 acc += norm2(u);
                 accB += norm2(v);
                 accC += (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+                accD += (double)u.x * (double)v.x + (double)u.y * (double)v.y;
             }
             const double A = team_sum(acc, sred, team, t);
             const double B = team_sum(accB, sred, team, t);
             const double C = team_sum(accC, sred, team, t);
+            const double D = team_sum(accD, sred, team, t);
             if (t == 0) {
-                double* p = ep.partial + (pslot * ntiles + x) * 3;
+                double* p = ep.partial + (pslot * ntiles + x) * 4;
                 p[0] = A;
                 p[1] = B;
                 p[2] = C;
+                p[3] = D;
             }
             const int32_t lo = ep.sup_off[x], hi = ep.sup_off[x + 1];
             for (int32_t q = lo + t; q < hi; q += 256) {
@@ -828,10 +837,11 @@ ring_pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const L
                 for (int j = 0; j < K; ++j)
                     if ((loc >> j) & 1u) gidx |= 1ull << pd.sbits[j];
                 const V u = aux[gidx];
-                double* row = ep.pair_sup + (e.rslot * ep.S + ep.sup_pos[q]) * 3;
+                double* row = ep.pair_sup + (e.rslot * ep.S + ep.sup_pos[q]) * 4;
                 row[0] = norm2(u);
                 row[1] = norm2(v);
                 row[2] = (double)u.y * (double)v.x - (double)u.x * (double)v.y;
+                row[3] = (double)u.x * (double)v.x + (double)u.y * (double)v.y;
             }
         } else {
 #pragma unroll
@@ -893,17 +903,23 @@ __global__ void finalize_dist_kernel(const int64_t* __restrict__ slots, int64_t 
 // slots[2*b] = result slot, slots[2*b+1] = partial slot; out[2r], out[2r+1].
 __global__ void finalize_pair_kernel(const int64_t* __restrict__ slots, int64_t ntiles, const double* __restrict__ partial,
                                      const double* __restrict__ pair_sup, int64_t S, const double* __restrict__ target,
-                                     double* __restrict__ out, int unit_norm) {
+                                     double* __restrict__ out, int unit_norm, const double* __restrict__ delta) {
     __shared__ double sred[32];
     const int64_t r = slots[2 * blockIdx.x], ps = slots[2 * blockIdx.x + 1];
-    double a = 0.0, b = 0.0, c = 0.0;
+    // the device Xi carries an extra global phase e^{i delta_r} relative to
+    // Psi0 (per-matrix phase normalisation): Psi0 conj(Xi_true) = z e^{-i delta}
+    // for the computed z, so Im(Psi0 conj Xi_true) = Im z cos delta - Re z sin delta
+    const double cd = cos(delta[r]), sd = sin(delta[r]);
+    double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
     for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) {
-        const double* p = partial + (ps * ntiles + i) * 3;
+        const double* p = partial + (ps * ntiles + i) * 4;
         a += p[0];
         b += p[1];
         c += p[2];
+        d += p[3];
     }
-    double A = block_sum(a, sred), B = block_sum(b, sred), C = block_sum(c, sred);
+    double A = block_sum(a, sred), B = block_sum(b, sred);
+    double C = block_sum(c, sred) * cd - block_sum(d, sred) * sd;
     if (unit_norm) {   // light-cone run: |Psi0| = |Xi| = 1 and Im<Psi0|Xi> = 0 exactly
         A = 1.0;
         B = 1.0;
@@ -912,9 +928,10 @@ __global__ void finalize_pair_kernel(const int64_t* __restrict__ slots, int64_t 
     const double tp = A + B - 2.0 * C, tm = A + B + 2.0 * C;
     double jp = 0.0, jm = 0.0, sp = 0.0, sm = 0.0;
     for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
-        const double* q = pair_sup + (r * S + s) * 3;
-        const double qp = (q[0] + q[1] - 2.0 * q[2]) / tp;
-        const double qm = (q[0] + q[1] + 2.0 * q[2]) / tm;
+        const double* q = pair_sup + (r * S + s) * 4;
+        const double im = q[2] * cd - q[3] * sd;
+        const double qp = (q[0] + q[1] - 2.0 * im) / tp;
+        const double qm = (q[0] + q[1] + 2.0 * im) / tm;
         jp += js_term(target[s], qp);
         jm += js_term(target[s], qm);
         sp += qp;
