@@ -52,6 +52,19 @@ def test_zigzag_block_owner():
     assert [qv.vqpu.rank_of_block(b, 1) for b in range(3)] == [0, 0, 0]
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_bench_blocks_keep_shift_pairs_whole(world):
+    """bench.py's pool (24 blocks per rank) on the 28q x 8L shift table
+    (2688 rows, rows 2k / 2k+1 = the +/- pair of parameter k): every block
+    holds whole pairs and every rank the same number of rows."""
+    rows = 2 * qv.ddcl_parameter_count(28, 8)
+    blocks = [b for b in qv.partition(rows, 24 * world) if b.size]
+    assert all(b.start % 2 == 0 and b.size % 2 == 0 for b in blocks)
+    per_rank = [sum(b.size for i, b in enumerate(blocks) if qv.vqpu.rank_of_block(i, world) == r)
+                for r in range(world)]
+    assert per_rank == [rows // world] * world
+
+
 @pytest.mark.parametrize("n_circuits,n_vqpus", [(10, 4), (7, 16), (2688, 16), (5, 1)])
 def test_execute_values_two_ranks(n_circuits, n_vqpus):
     manager = mp.Manager()
