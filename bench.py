@@ -298,7 +298,7 @@ def run_reference(args):
 
 
 POINTS = 1024   # config 3's batch of data points
-BLOCKS_PER_RANK = 24   # vQPU blocks per GPU under torchrun (see main)
+BLOCKS_PER_RANK = 24   # vQPU blocks per GPU under torchrun, non-QCL workloads (see main)
 
 # the paper's published strong-scaling fits (Table 3,
 # PAPER.md:303-325), log10(seconds) = a * log2(GPUs) + b, V100 + cuStateVec,
@@ -406,12 +406,19 @@ def main():
         def step():
             return qv.mcvqe_gradient(ham, mspec, pool, backend_factory=_Factory(device, precision))
 
-    # 24 vQPU blocks per GPU, dealt to ranks in zigzag order (vqpu.rank_of_block)
-    # so every rank gets parameters from every depth; each rank runs its blocks
-    # as one batch sharing one trunk.  24 (not 8) balances the ranks better --
-    # tools/shard_probe.py, 28q x 8L split 8 ways: max shard 4.72 s vs 4.99 s --
-    # and keeps the 28q x 8L blocks an even number of rows (no ± pair split)
-    pool = qv.VqpuPoolConfig(n_virtual_qpus=1 if world == 1 else BLOCKS_PER_RANK * world)
+    # vQPU blocks dealt to ranks in zigzag order (vqpu.rank_of_block) so every
+    # rank gets parameters from every depth; each rank runs its blocks as one
+    # batch sharing one trunk.  QCL gradients: one vQPU per parameter (its ±
+    # shift pair), the finest split that never cuts a pair -- tools/shard_probe.py,
+    # 28q x 8L split 8 ways: max shard 4.62 s, vs 4.72 s with 24 blocks per rank
+    # and 4.99 s with 8.  Other workloads: BLOCKS_PER_RANK blocks per rank.
+    if world == 1:
+        n_vqpus = 1
+    elif kind == "qcl":
+        n_vqpus = qv.ddcl_parameter_count(n, layers)
+    else:
+        n_vqpus = BLOCKS_PER_RANK * world
+    pool = qv.VqpuPoolConfig(n_virtual_qpus=n_vqpus)
     engine = native.engine(device, precision)
 
     def barrier():

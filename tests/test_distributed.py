@@ -1,5 +1,5 @@
 """Multi-process path of the virtual-QPU pool on CPU (torch.distributed,
-gloo, world size 2): block b runs on rank b mod W, per-circuit scalars are
+gloo, world size 2): block b runs on rank `rank_of_block(b, W)` (zigzag), per-circuit scalars are
 exchanged with one padded all-gather, every rank ends with the full vector
 in batch order.  A stub backend stands in for the GPU (the exchange logic is
 what is under test; the B200 path runs the same code with NCCL)."""
@@ -54,11 +54,12 @@ def test_zigzag_block_owner():
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_bench_blocks_keep_shift_pairs_whole(world):
-    """bench.py's pool (24 blocks per rank) on the 28q x 8L shift table
-    (2688 rows, rows 2k / 2k+1 = the +/- pair of parameter k): every block
-    holds whole pairs and every rank the same number of rows."""
-    rows = 2 * qv.ddcl_parameter_count(28, 8)
-    blocks = [b for b in qv.partition(rows, 24 * world) if b.size]
+    """bench.py's QCL pool (one vQPU per parameter) on the 28q x 8L shift
+    table (2688 rows, rows 2k / 2k+1 = the +/- pair of parameter k): every
+    block is one whole pair and every rank gets the same number of rows."""
+    n_theta = qv.ddcl_parameter_count(28, 8)
+    rows = 2 * n_theta
+    blocks = [b for b in qv.partition(rows, n_theta) if b.size]
     assert all(b.start % 2 == 0 and b.size % 2 == 0 for b in blocks)
     per_rank = [sum(b.size for i, b in enumerate(blocks) if qv.vqpu.rank_of_block(i, world) == r)
                 for r in range(world)]
