@@ -375,6 +375,7 @@ def main():
 
     import paper_2406_03466_b200 as qv
     from paper_2406_03466_b200 import native
+    from paper_2406_03466_b200.vqpu import rank_local
 
     kind, n, layers, precision, desc = WORKLOADS[args.workload]
     s = args.seed
@@ -396,8 +397,11 @@ def main():
         def step():
             if kind == "qcl_fwd":
                 return _Step(POINTS, qv.ddcl_forward_losses(specs, fwd_backend))
-            grads = [qv.ddcl_gradient(sp, one_pool, backend_factory=_Factory(device, precision)).gradient
-                     for sp in specs]
+            # the points are already dealt to ranks: each rank's gradients run
+            # on its own GPU with no collective (vqpu.rank_local)
+            with rank_local():
+                grads = [qv.ddcl_gradient(sp, one_pool, backend_factory=_Factory(device, precision)).gradient
+                         for sp in specs]
             return _Step(circuits_per_step(kind, n, layers), np.concatenate(grads))
     else:
         ham = qv.aiem_hamiltonian(qv.random_aiem_coefficients(n, s))

@@ -26,6 +26,7 @@ from __future__ import annotations
 import itertools
 import math
 import threading
+from operator import attrgetter, itemgetter
 from dataclasses import dataclass
 from typing import Callable, Iterable, Mapping, Protocol, Sequence
 
@@ -74,28 +75,54 @@ class Accelerator(Protocol):
 # ---------------------------------------------------------------------------
 # lowering: Circuit objects -> C-ABI gate arrays
 
-def _foreign_arrays(circuit) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
-    """Gate arrays of any reference-shaped circuit (duck-typed: .gates with
-    .kind.value / .targets / .angle), e.g. a `qvirt.Circuit`."""
-    gates = circuit.gates
-    count = len(gates)
-    kinds = np.empty(count, np.uint8)
-    q0 = np.zeros(count, np.int32)
-    q1 = np.full(count, -1, np.int32)
-    ang = np.zeros(count, np.float64)
-    for i, g in enumerate(gates):
-        kinds[i] = CODE_BY_VALUE[g.kind.value]
-        t = g.targets
-        if t:
-            q0[i] = t[0]
-            if len(t) > 1:
-                q1[i] = t[1]
-        a = g.angle
-        if a is not None:
-            if isinstance(a, str):
-                raise ValueError(f"unbound parameter {a!r}; bind before executing")
-            ang[i] = a
-    return kinds, q0, q1, ang
+_KIND_OF = attrgetter("kind")
+_TARGETS_OF = attrgetter("targets")
+_ANGLE_OF = attrgetter("angle")
+
+
+class _ForeignTopology:
+    """Gate arrays of one reference-shaped gate list (duck-typed: .gates with
+    .kind.value / .targets / .angle, e.g. a `qvirt.Circuit`), reused for every
+    later circuit with the same kinds and targets (a parameter-shift batch is
+    2 N_theta bindings of one template, gradients.py:33-46).  The per-circuit
+    work is three C-level passes over the gate tuple (kinds, targets, and the
+    angles of the rotation gates) instead of a Python loop per gate."""
+
+    def __init__(self, gates):
+        self.kind_list = list(map(_KIND_OF, gates))
+        self.target_list = list(map(_TARGETS_OF, gates))
+        count = len(gates)
+        self.kinds = np.fromiter((CODE_BY_VALUE[k.value] for k in self.kind_list), np.uint8, count)
+        self.q0 = np.fromiter((t[0] if t else 0 for t in self.target_list), np.int32, count)
+        self.q1 = np.fromiter((t[1] if len(t) > 1 else -1 for t in self.target_list), np.int32, count)
+        angles = list(map(_ANGLE_OF, gates))
+        self.rot = np.fromiter((i for i, a in enumerate(angles) if a is not None), np.int64)
+        self.pick = itemgetter(*self.rot.tolist()) if self.rot.size > 1 else None
+
+    def matches(self, gates) -> bool:
+        return (len(gates) == len(self.kind_list) and list(map(_KIND_OF, gates)) == self.kind_list
+                and list(map(_TARGETS_OF, gates)) == self.target_list)
+
+    def angles(self, gates) -> np.ndarray:
+        ang = np.zeros(len(self.kind_list), np.float64)
+        if self.rot.size == 0:
+            return ang
+        chosen = self.pick(gates) if self.pick is not None else (gates[int(self.rot[0])],)
+        try:
+            ang[self.rot] = np.fromiter(map(_ANGLE_OF, chosen), np.float64, self.rot.size)
+        except (TypeError, ValueError):
+            bad = next(a for a in map(_ANGLE_OF, chosen) if not isinstance(a, (int, float)))
+            raise ValueError(f"unbound parameter {bad!r}; bind before executing") from None
+        return ang
+
+
+def _foreign_arrays(circuit, topo: _ForeignTopology | None = None):
+    """(kinds, q0, q1, angles) of a reference-shaped circuit, and the
+    topology they came from (reused when `topo` matches)."""
+    gates = tuple(circuit.gates)
+    if topo is None or not topo.matches(gates):
+        topo = _ForeignTopology(gates)
+    return (topo.kinds, topo.q0, topo.q1, topo.angles(gates)), topo
 
 
 def lower_batch(circuits: Sequence) -> native.LoweredBatch:
@@ -117,6 +144,7 @@ def lower_batch(circuits: Sequence) -> native.LoweredBatch:
             angles = lw.gate_angles(values)
             return native.LoweredBatch(len(circuits), True, lw.kinds.shape[0], None, lw.kinds, lw.q0, lw.q1, angles)
     parts = []
+    topo = None
     for c in circuits:
         if isinstance(c, Circuit) and not c.is_parameterized:
             if c._rows is not None:
@@ -126,7 +154,8 @@ def lower_batch(circuits: Sequence) -> native.LoweredBatch:
                 lw = c.lowering()
                 parts.append((lw.kinds, lw.q0, lw.q1, lw.literal))
         else:
-            parts.append(_foreign_arrays(c))
+            arrays, topo = _foreign_arrays(c, topo)
+            parts.append(arrays)
     counts = np.fromiter((p[0].shape[0] for p in parts), np.int64, len(parts))
     offsets = np.zeros(len(parts) + 1, np.int64)
     np.cumsum(counts, out=offsets[1:])
@@ -150,6 +179,11 @@ def support_indices(support, n_qubits: int) -> np.ndarray:
     distribution (bitstring keys), bitstrings, or integer indices."""
     items = list(support.keys()) if isinstance(support, Mapping) else list(support)
     if items and all(isinstance(item, str) for item in items):
+        # every key must be n bits wide: a joined length check alone would let
+        # keys of mixed widths ('0', '111' for n = 2) parse into a wrong support
+        bad = next((it for it in items if len(it) != n_qubits), None)
+        if bad is not None:
+            raise ValueError(f"bad support bitstring {bad!r} for {n_qubits} qubits")
         # vectorised parse: one uint8 row per bitstring, most significant bit first
         try:
             raw = np.frombuffer("".join(items).encode("ascii"), dtype=np.uint8)

@@ -26,7 +26,7 @@ PRODUCT = PKG / "libqvb200.so"
 PLANCHECK = PKG / "libqvb200_plan.so"
 
 PRODUCT_SOURCES = [CSRC / "qvb200.cu", CSRC / "plan.cpp"]
-PRODUCT_DEPS = PRODUCT_SOURCES + [CSRC / "kernels.cuh", CSRC / "sampling.cuh", CSRC / "plan.hpp",
+PRODUCT_DEPS = PRODUCT_SOURCES + [CSRC / "kernels.cuh", CSRC / "sampling.cuh", CSRC / "plan.hpp", CSRC / "tma_pass.cuh",
                                   INCLUDE / "qvb200.h"]
 PLANCHECK_SOURCES = [CSRC / "plancheck.cpp", CSRC / "plan.cpp"]
 PLANCHECK_DEPS = PLANCHECK_SOURCES + [CSRC / "plan.hpp"]
@@ -52,17 +52,6 @@ def build_product(force: bool = False, verbose_ptxas: bool = False) -> Path:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
     return PRODUCT
-
-
-TRACE = PKG / "libqvb200_trace.so"
-
-
-def build_trace(force: bool = False) -> Path:
-    """Debug build with per-phase clock64() tracing (tools/trace_pass.py)."""
-    if force or _stale(TRACE, PRODUCT_DEPS):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-DQV_TRACE",
-              "-cudart", "static", f"-I{INCLUDE}", f"-I{CSRC}", "-o", TRACE, *PRODUCT_SOURCES])
-    return TRACE
 
 
 def build_variant(name: str, defines: list[str], force: bool = False) -> Path:

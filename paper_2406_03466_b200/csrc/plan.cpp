@@ -10,14 +10,11 @@
 //   RX = [[c,-is],[-is,c]];  CZ(a,b) = H_b CNOT(a,b) H_b.
 #include "plan.hpp"
 
-#ifndef QV_SWZ_TMA
-#define QV_SWZ_TMA 0
-#endif
-
 #include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <functional>
 #include <stdexcept>
 
 namespace qvb {
@@ -136,6 +133,7 @@ struct GroupBuilder {
     int k, beta;
     int rbits;             // register bits per group (reg_bits(precision))
     int amp_shift;         // log2(bytes per amplitude): 4 complex128, 3 complex64
+    bool tma = false;      // TMA 128-byte swizzle instead of the full bank fold
     uint16_t col[16];      // logical-bit -> slot column (before swizzle): the map Q
     std::vector<std::pair<int, int>> open;  // (logical bit, pass-local matrix index)
 
@@ -147,11 +145,14 @@ struct GroupBuilder {
     std::vector<Pending> pending;
 
     uint16_t swz(uint32_t v) const {   // bank swizzle, GF(2)-linear
-        uint32_t r = v;
-        // QV_SWZ_TMA (experiment): fold only bits beta..2*beta-1, the pattern of
-        // TMA's 128-byte swizzle (16-byte chunk ^= row index mod 8)
-        const int top = QV_SWZ_TMA ? std::min(k, 2 * beta) : k;
-        for (int j = beta; j < top; ++j)
+        if (tma) {
+            // TMA SWIZZLE_128B: the 16-byte chunk (byte-address bits 4-6) is
+            // XORed with the 128-byte row index mod 8 (bits 7-9)
+            const int chunk = 4 - amp_shift, row = 7 - amp_shift;
+            return (uint16_t)(v ^ (((v >> row) & 7u) << chunk));
+        }
+        uint32_t r = v;   // every bit above the bank bits folds into them
+        for (int j = beta; j < k; ++j)
             if ((v >> j) & 1u) r ^= 1u << (j % beta);
         return (uint16_t)r;
     }
@@ -296,29 +297,28 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
     } else {
         plan.passes = select_passes(n, k, coalesce_bits(precision), plan.ops);
     }
-    // Bank model of one pass's groups (warp 0; the other warps differ by a
-    // constant XOR): wavefronts of its loads + stores, 128-bit (complex128)
-    // or 64-bit (complex64) accesses.
-    auto bank_wavefronts = [&](const PassDesc& d) {
-        const int sh = precision == 0 ? 4 : 3, rows = precision == 0 ? 8 : 16;
+    // Bank model of one warp's accesses (warp 0; the other warps differ by a
+    // constant XOR): wavefronts of one register set, 128-bit (complex128) or
+    // 64-bit (complex64) accesses.
+    const int sh = precision == 0 ? 4 : 3, rows = precision == 0 ? 8 : 16;
+    const int R = reg_bits(precision), tbits = k - R;
+    auto access_wf = [&](const uint32_t* combo, const uint32_t* tcol) {
         int64_t wf = 0;
-        for (int g = d.g0; g < d.g0 + d.ng; ++g) {
-            const GroupDesc& G = plan.groups[g];
-            for (int j = 0; j < (1 << reg_bits(precision)); ++j) {
-                int count[16] = {0};
-                for (int lane = 0; lane < 32; ++lane) {
-                    uint32_t base = 0;
-                    for (int m = 0; m < 5 && m < k - reg_bits(precision); ++m)
-                        if ((lane >> m) & 1) base ^= G.tcol[m];
-                    ++count[((base ^ G.combo[j]) >> sh) & (rows - 1)];
-                }
-                wf += 2 * *std::max_element(count, count + rows);
+        for (int j = 0; j < (1 << R); ++j) {
+            int count[16] = {0};
+            for (int lane = 0; lane < 32; ++lane) {
+                uint32_t base = 0;
+                for (int m = 0; m < 5 && m < tbits; ++m)
+                    if ((lane >> m) & 1) base ^= tcol[m];
+                ++count[((base ^ combo[j]) >> sh) & (rows - 1)];
             }
+            wf += *std::max_element(count, count + rows);
         }
         return wf;
     };
+    const int c = coalesce_bits(precision);
     for (auto& pp : plan.passes) {
-        auto build_pass = [&](const uint16_t* init_cols) {
+        auto build_pass = [&](const uint16_t* init_cols, bool tma) {
             PassDesc d;
             std::memset(&d, 0, sizeof(d));
             d.k = k;
@@ -331,12 +331,12 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
                 for (int b = 0; b < n; ++b)
                     if (logical_of[b] < 0) d.obits[o++] = (uint8_t)b;
             }
-            const int R = reg_bits(precision);
             GroupBuilder gb;
             gb.k = k;
             gb.beta = beta;
             gb.rbits = R;
             gb.amp_shift = precision == 0 ? 4 : 3;
+            gb.tma = tma;
             for (int j = 0; j < 16; ++j) gb.col[j] = init_cols[j];
             for (int j = 0; j < k; ++j) d.swz[j] = gb.phys(j);
             d.g0 = (int)plan.groups.size();
@@ -423,39 +423,137 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
             pp.n_groups = d.ng;
             pp.n_mats = d.nm;
             plan.pdesc.push_back(d);
-            };
+        };
+        // Store map of the last group (TMA layout) and the bank cost of a pass
+        // built on a TMA layout; tl.ok = 0 if it has no register group.
+        auto finish_tma = [&](TmaLayout& tl) {
+            const PassDesc& d = plan.pdesc.back();
+            int64_t wf = 0;
+            for (int g = d.g0; g < d.g0 + d.ng; ++g) {
+                wf += access_wf(plan.groups[g].combo, plan.groups[g].tcol);
+                if (g + 1 < d.g0 + d.ng) wf += access_wf(plan.groups[g].combo, plan.groups[g].tcol);
+            }
+            tl.ok = d.ng > 0 ? 1 : 0;
+            if (d.ng > 0) {
+                // physical slot p holds, at the end of the pass, logical fin^-1(p);
+                // the last group writes it to the TMA slot of that logical index
+                const int shift = precision == 0 ? 4 : 3;
+                std::vector<uint32_t> inv((size_t)1 << k);
+                for (uint32_t l = 0; l < (1u << k); ++l) inv[apply_cols(d.fin, k, l)] = l;
+                const GroupDesc& G = plan.groups[d.g0 + d.ng - 1];
+                for (int j = 0; j < (1 << R); ++j)
+                    tl.wcombo[j] = (uint32_t)apply_cols(d.swz, k, inv[G.combo[j] >> shift]) << shift;
+                for (int mm = 0; mm < tbits && mm < 11; ++mm)
+                    tl.wtcol[mm] = (uint32_t)apply_cols(d.swz, k, inv[G.tcol[mm] >> shift]) << shift;
+                wf += access_wf(tl.wcombo, tl.wtcol);
+            }
+            tl.wavefronts = wf;
+        };
         uint16_t ident[16];
         for (int j = 0; j < 16; ++j) ident[j] = (uint16_t)(j < k ? 1u << j : 0);
-        if (!QV_SWZ_TMA || plan.single_tile || beta != 3 || k < 2 * beta + 1) {   // complex128 rows only
-            build_pass(ident);
+        if (plan.single_tile) {
+            build_pass(ident, false);
+            plan.tma.push_back(TmaLayout{});
             continue;
         }
-        // QV_SWZ_TMA: the tile bits at physical positions beta..2*beta-1 are
-        // the ones the 128-byte TMA swizzle folds into the bank bits; try every
-        // choice of them and keep the layout with the fewest bank wavefronts
-        uint16_t best[16];
-        int64_t best_wf = -1;
-        for (int a = beta; a < k; ++a)
-            for (int b = a + 1; b < k; ++b)
-                for (int c = b + 1; c < k; ++c) {
-                    uint16_t cols[16] = {0};
-                    int next = 2 * beta;
-                    for (int j = 0; j < k; ++j) {
-                        int pos = j < beta ? j : j == a ? beta : j == b ? beta + 1 : j == c ? beta + 2 : next++;
-                        cols[j] = (uint16_t)(1u << pos);
-                    }
-                    const size_t g0 = plan.groups.size(), m0 = plan.mat_op.size(), p0 = plan.pdesc.size();
-                    build_pass(cols);
-                    const int64_t wf = bank_wavefronts(plan.pdesc.back());
-                    plan.groups.resize(g0);
-                    plan.mat_op.resize(m0);
-                    plan.pdesc.resize(p0);
-                    if (best_wf < 0 || wf < best_wf) {
-                        best_wf = wf;
-                        std::memcpy(best, cols, sizeof(best));
-                    }
+        // Candidate TMA layouts: the tile bits above the low `c` split into <= 3
+        // pieces of <= 8 consecutive global bits, in any order.  Only the bits
+        // that land in the swizzled row positions c..c+2 matter for the banks,
+        // so one candidate (the fewest pieces) is built per choice of them.
+        struct Piece { int lo, len; };
+        std::vector<Piece> runs;
+        for (int b : pp.S) {
+            if (b < c) continue;
+            if (!runs.empty() && runs.back().lo + runs.back().len == b) ++runs.back().len;
+            else runs.push_back({b, 1});
+        }
+        std::vector<std::vector<Piece>> cands;
+        std::vector<uint64_t> keys;
+        std::vector<Piece> acc;
+        std::function<void(size_t)> per_run;
+        std::function<void(size_t, int, int)> split = [&](size_t r, int start, int end) {
+            if (start == end) { per_run(r + 1); return; }
+            for (int len = 1; len <= 8 && start + len <= end; ++len) {
+                acc.push_back({start, len});
+                if (acc.size() <= 3) split(r, start + len, end);
+                acc.pop_back();
+            }
+        };
+        per_run = [&](size_t r) {
+            if (r < runs.size()) { split(r, runs[r].lo, runs[r].lo + runs[r].len); return; }
+            std::vector<int> idx(acc.size());
+            for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+            do {
+                std::vector<Piece> order;
+                uint64_t key = 0;
+                int placed = 0;
+                for (int i : idx) {
+                    order.push_back(acc[i]);
+                    for (int b = acc[i].lo; b < acc[i].lo + acc[i].len && placed < 3; ++b, ++placed)
+                        key = (key << 8) | (uint64_t)(b + 1);
                 }
-        build_pass(best);
+                auto it = std::find(keys.begin(), keys.end(), key);
+                if (it == keys.end()) { keys.push_back(key); cands.push_back(order); }
+                else if (cands[it - keys.begin()].size() > order.size()) cands[it - keys.begin()] = order;
+            } while (std::next_permutation(idx.begin(), idx.end()));
+        };
+        const bool low_ok = k > c && [&]() {
+            for (int b = 0; b < c; ++b)
+                if (std::find(pp.S.begin(), pp.S.end(), b) == pp.S.end()) return false;
+            return true;
+        }();
+        if (low_ok) per_run(0);
+        auto layout_of = [&](const std::vector<Piece>& order, uint16_t* cols, TmaLayout& tl) {
+            std::vector<int> pos_of_bit(64, -1);
+            int pos = 0;
+            for (int b = 0; b < c; ++b) pos_of_bit[b] = pos++;
+            for (const Piece& pc : order)
+                for (int b = pc.lo; b < pc.lo + pc.len; ++b) pos_of_bit[b] = pos++;
+            for (int j = 0; j < 16; ++j) cols[j] = j < k ? (uint16_t)(1u << pos_of_bit[pp.S[j]]) : 0;
+            std::vector<char> local(64, 0);
+            for (int b : pp.S) local[b] = 1;
+            auto span_of = [&](int lo, int len) {   // the piece + outer bits up to the next tile bit
+                int e = lo + len;
+                while (e < n && !local[e]) ++e;
+                return e - lo;
+            };
+            tl.ndim = 1 + (int)order.size();
+            tl.lo[0] = 0;
+            tl.box[0] = c;
+            tl.span[0] = span_of(0, c);
+            for (size_t i = 0; i < order.size(); ++i) {
+                tl.lo[i + 1] = order[i].lo;
+                tl.box[i + 1] = order[i].len;
+                tl.span[i + 1] = span_of(order[i].lo, order[i].len);
+            }
+        };
+        TmaLayout best_tl;
+        uint16_t best_cols[16];
+        int64_t best_wf = -1;
+        for (const auto& cand : cands) {
+            uint16_t cols[16];
+            TmaLayout tl;
+            layout_of(cand, cols, tl);
+            const size_t g0 = plan.groups.size(), m0 = plan.mat_op.size(), p0 = plan.pdesc.size();
+            build_pass(cols, true);
+            finish_tma(tl);
+            plan.groups.resize(g0);
+            plan.mat_op.resize(m0);
+            plan.pdesc.resize(p0);
+            if (tl.ok && (best_wf < 0 || tl.wavefronts < best_wf)) {
+                best_wf = tl.wavefronts;
+                best_tl = tl;
+                std::memcpy(best_cols, cols, sizeof(best_cols));
+            }
+        }
+        if (best_wf >= 0) {
+            build_pass(best_cols, true);
+            finish_tma(best_tl);
+            plan.tma.push_back(best_tl);
+        } else {
+            build_pass(ident, false);
+            plan.tma.push_back(TmaLayout{});
+        }
     }
     return plan;
 }

@@ -115,6 +115,33 @@ struct PassPlan {
     int n_mats = 0;
 };
 
+// Tensor-memory-accelerator layout of a multi-tile pass (tma_pass.cuh).
+//
+// The state batch is viewed as a <= 5-D tensor: each index dimension is one
+// "piece" of the pass's tile bits (a run of consecutive global bits, <= 8 of
+// them so the box stays <= 256 elements) together with the outer bits above
+// it up to the next piece; the last dimension is the state slot.  A tile is
+// then ONE box of that tensor, and the box lands in shared memory in piece
+// order (dimension 0 = the low `coalesce` bits, a 128-byte row) under TMA's
+// 128-byte swizzle (16-byte chunk ^= row mod 8).  The planner picks the pieces
+// and their order (which tile bits sit in the swizzled row positions) to
+// minimise shared-memory bank wavefronts of the pass's register groups, and
+// the pass's groups are built on that layout, so the TMA load needs no
+// re-layout.  CNOTs folded into the slot maps leave the tile permuted at the
+// end of the pass; the LAST register group therefore writes its amplitudes
+// back in the TMA layout (wcombo / wtcol) and the TMA store reads the same
+// box layout.
+struct TmaLayout {
+    int32_t ok = 0;             // the pass can run on the TMA kernel
+    int32_t ndim = 0;           // index dimensions, shared-memory order (<= 4)
+    int32_t lo[4] = {0, 0, 0, 0};    // lowest global bit of each dimension
+    int32_t span[4] = {0, 0, 0, 0};  // global bits the dimension covers
+    int32_t box[4] = {0, 0, 0, 0};   // tile bits of the dimension (box = 2^box)
+    uint32_t wcombo[16] = {0};  // last group: byte offset of register j in the TMA layout
+    uint32_t wtcol[11] = {0};   // last group: byte offset of thread bit m in the TMA layout
+    int64_t wavefronts = 0;     // bank model of the chosen layout (tools / tests)
+};
+
 struct Plan {
     int n = 0;
     int k = 0;               // tile bits
@@ -124,6 +151,7 @@ struct Plan {
     std::vector<int> mat_op;         // matrix slot -> fused op (slots ordered pass by pass)
     std::vector<PassPlan> passes;
     std::vector<PassDesc> pdesc;
+    std::vector<TmaLayout> tma;      // per pass
     std::vector<GroupDesc> groups;
     int n_slots() const { return (int)mat_op.size(); }
 };

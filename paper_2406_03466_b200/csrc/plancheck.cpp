@@ -30,12 +30,44 @@ Topology make_topo(int n, int64_t ng, const uint8_t* kinds, const int32_t* q0, c
 }
 }  // namespace
 
-extern "C" {
+// Shared-memory slot (in amplitudes) of global index g inside the TMA box of a
+// pass, computed from the layout's tensor dimensions exactly as the TMA unit
+// places a box (dimension 0 fastest, each dimension's box bits packed above
+// the previous ones) followed by the 128-byte swizzle of the byte address
+// (16-byte chunk ^= 128-byte row mod 8).  Independent of the planner's slot
+// columns, so the interpreter checks them against the hardware's layout.
+static uint32_t tma_slot(const TmaLayout& tl, int precision, uint64_t g) {
+    uint32_t e = 0;
+    int at = 0;
+    for (int d = 0; d < tl.ndim; ++d) {
+        e |= (uint32_t)((g >> tl.lo[d]) & ((1ull << tl.box[d]) - 1)) << at;
+        at += tl.box[d];
+    }
+    const int shift = precision == 0 ? 4 : 3;
+    uint32_t byte = e << shift;
+    byte ^= ((byte >> 7) & 7u) << 4;
+    return byte >> shift;
+}
+
+// Outer offset reassembled from the tensor coordinates of a tile (what the
+// TMA producer computes); must equal the tile's outer offset.
+static uint64_t tma_outer(const TmaLayout& tl, uint64_t outer) {
+    uint64_t r = 0;
+    for (int d = 0; d < tl.ndim; ++d) {
+        const uint64_t coord = (outer >> tl.lo[d]) & ((1ull << tl.span[d]) - 1);
+        r |= coord << tl.lo[d];
+    }
+    return r;
+}
 
 // Final state of one circuit after running its plan; out = 2 * 2^n doubles.
-// Returns the number of passes, or -1 on error.
-int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
-                 const double* angles, int precision, int max_tile_bits, double* out) {
+// tma = 1 interprets every pass with a TMA layout as tma_pass_kernel does
+// (load and store through the TMA box layout, the last register group
+// writing in that layout); tma = 0 as pass_kernel does.
+// Returns the number of passes, -1 on error, -2 on a warp-locality
+// violation, -3 on a TMA layout inconsistency.
+static int simulate_impl(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                         const double* angles, int precision, int max_tile_bits, double* out, int tma) {
     try {
         const Topology topo = make_topo(n, n_gates, kinds, q0, q1);
         const Plan plan = build_plan(topo, precision, max_tile_bits);
@@ -46,23 +78,32 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
         const size_t dim = (size_t)1 << std::max(n, k);
         std::vector<cd> st(dim, cd(0, 0)), tile((size_t)1 << k);
         st[0] = 1.0;
-        for (const PassDesc& pd : plan.pdesc) {
+        for (size_t p = 0; p < plan.pdesc.size(); ++p) {
+            const PassDesc& pd = plan.pdesc[p];
+            const TmaLayout& tl = plan.tma[p];
+            const bool use_tma = tma && tl.ok;
             const int64_t ntiles = plan.single_tile ? 1 : (1ll << pd.n_outer);
             for (int64_t x = 0; x < ntiles; ++x) {
                 uint64_t outer = 0;
                 for (int j = 0; j < pd.n_outer; ++j)
                     if ((x >> j) & 1) outer |= 1ull << pd.obits[j];
+                if (use_tma && tma_outer(tl, outer) != outer) return -3;
                 for (int tid = 0; tid < nt; ++tid) {
                     uint32_t ts = 0;
                     uint64_t tg = 0;
                     for (int j = 0; j < tb; ++j)
                         if ((tid >> j) & 1) { ts ^= pd.swz[j]; tg |= 1ull << pd.sbits[j]; }
-                    for (int it = 0; it < NA; ++it) tile[ts ^ pd.swz_hi[it]] = st[outer | tg | pd.g_hi[it]];
+                    for (int it = 0; it < NA; ++it) {
+                        const uint64_t g = outer | tg | pd.g_hi[it];
+                        if (use_tma && tma_slot(tl, precision, g) != (ts ^ pd.swz_hi[it])) return -3;
+                        tile[ts ^ pd.swz_hi[it]] = st[g];
+                    }
                 }
                 const int sh = precision == 0 ? 4 : 3;   // descriptors hold byte offsets
                 // warp-local segments: without a CTA barrier, every warp must touch
                 // exactly the slots it touched in the previous group
                 std::vector<std::vector<uint32_t>> prev_sets;
+                std::vector<std::vector<cd>> groups_out(nt);
                 for (int g = pd.g0; g < pd.g0 + pd.ng; ++g) {
                     const GroupDesc& G = plan.groups[g];
                     const int nwarps = (nt + 31) / 32;
@@ -93,7 +134,19 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
                                 a[j | (1 << r)] = m10 * u + m11 * v;
                             }
                         }
-                        for (int j = 0; j < NA; ++j) tile[(base ^ G.combo[j]) >> sh] = a[j];
+                        groups_out[tid].assign(a, a + NA);
+                    }
+                    // every thread has read its registers before any writes (the
+                    // TMA kernel's last group writes after a compute barrier)
+                    const bool last_tma = use_tma && g == pd.g0 + pd.ng - 1;
+                    for (int tid = 0; tid < nt; ++tid) {
+                        uint32_t base = 0, wbase = 0;
+                        for (int m = 0; m < tb; ++m)
+                            if ((tid >> m) & 1) { base ^= G.tcol[m]; wbase ^= tl.wtcol[m]; }
+                        for (int j = 0; j < NA; ++j) {
+                            const uint32_t at = last_tma ? (wbase ^ tl.wcombo[j]) : (base ^ G.combo[j]);
+                            tile[at >> sh] = groups_out[tid][j];
+                        }
                     }
                 }
                 for (int tid = 0; tid < nt; ++tid) {
@@ -101,11 +154,45 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
                     uint64_t tg = 0;
                     for (int j = 0; j < tb; ++j)
                         if ((tid >> j) & 1) { fs ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
-                    for (int it = 0; it < NA; ++it) st[outer | tg | pd.g_hi[it]] = tile[fs ^ pd.fin_hi[it]];
+                    for (int it = 0; it < NA; ++it) {
+                        const uint64_t g = outer | tg | pd.g_hi[it];
+                        st[g] = use_tma ? tile[tma_slot(tl, precision, g)] : tile[fs ^ pd.fin_hi[it]];
+                    }
                 }
             }
         }
         for (size_t i = 0; i < ((size_t)1 << n); ++i) { out[2 * i] = st[i].real(); out[2 * i + 1] = st[i].imag(); }
+        return (int)plan.pdesc.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+extern "C" {
+
+int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                 const double* angles, int precision, int max_tile_bits, double* out) {
+    return simulate_impl(n, n_gates, kinds, q0, q1, angles, precision, max_tile_bits, out, 0);
+}
+
+int qvp_simulate_tma(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                     const double* angles, int precision, int max_tile_bits, double* out) {
+    return simulate_impl(n, n_gates, kinds, q0, q1, angles, precision, max_tile_bits, out, 1);
+}
+
+// TMA layout of every pass: per pass 4 int64 (ok, ndim, wavefronts, ng);
+// returns the pass count or -1.
+int qvp_plan_tma(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1, int precision,
+                 int max_tile_bits, int64_t* out, int32_t cap) {
+    try {
+        const Topology topo = make_topo(n, n_gates, kinds, q0, q1);
+        const Plan plan = build_plan(topo, precision, max_tile_bits);
+        for (size_t p = 0; p < plan.pdesc.size() && (int32_t)p < cap; ++p) {
+            out[4 * p] = plan.tma[p].ok;
+            out[4 * p + 1] = plan.tma[p].ndim;
+            out[4 * p + 2] = plan.tma[p].wavefronts;
+            out[4 * p + 3] = plan.pdesc[p].ng;
+        }
         return (int)plan.pdesc.size();
     } catch (const std::exception&) {
         return -1;

@@ -33,6 +33,7 @@
 #include "kernels.cuh"
 #include "plan.hpp"
 #include "sampling.cuh"
+#include "tma_pass.cuh"
 #include "qvb200.h"
 
 namespace qvb {
@@ -305,7 +306,7 @@ using PassFn = void (*)(const PassDesc, const GroupDesc*, const LaunchEntry*, in
 
 template <typename T, int... TBs>
 constexpr std::array<PassFn<T>, sizeof...(TBs)> pass_table(std::integer_sequence<int, TBs...>) {
-    return {{&pass_kernel<T, TBs, false, 0>...}};
+    return {{&pass_kernel<T, TBs, 0>...}};
 }
 // TB = tile bits - 4: 0..8 for complex128 (k <= 12), 0..9 for complex64 (k <= 13)
 template <typename T>
@@ -313,121 +314,151 @@ const std::array<PassFn<T>, 10>& pass_kernels() {
     static const std::array<PassFn<T>, 10> table = pass_table<T>(std::make_integer_sequence<int, 10>{});
     return table;
 }
-// double-buffered variant used for multi-tile states (widest tile)
 template <typename T>
 constexpr int multi_tile_tb() {
     return max_tile_bits(sizeof(T) == 8 ? 0 : 1) - reg_bits(sizeof(T) == 8 ? 0 : 1);
 }
-// Double buffering (next tile streaming in behind the current one's math)
-// needs two widest tiles in shared memory and so leaves room for only one CTA
-// per SM.  Off by default: measured on B200 (28q x 8L gradient), two
-// independent single-buffered CTAs per SM -- one loading or storing while the
-// other computes -- are 13% faster (52.7 s vs 60.5 s).
-#ifndef QV_DOUBLE_BUFFER
-#define QV_DOUBLE_BUFFER 0
-#endif
-template <typename T>
-constexpr bool multi_tile_db() {
-    return QV_DOUBLE_BUFFER && (sizeof(typename Cx<T>::V) << max_tile_bits(sizeof(T) == 8 ? 0 : 1)) <= 96 * 1024;
-}
-// multi-tile launches (widest tile): deferred stores, optional double buffer
+// multi-tile launches (widest tile): deferred stores / shift-pair epilogue
 template <typename T>
 PassFn<T> pass_kernel_multi(bool pair) {
-    return pair ? &pass_kernel<T, multi_tile_tb<T>(), multi_tile_db<T>(), 2>
-                : &pass_kernel<T, multi_tile_tb<T>(), multi_tile_db<T>(), 1>;
+    return pair ? &pass_kernel<T, multi_tile_tb<T>(), 2> : &pass_kernel<T, multi_tile_tb<T>(), 1>;
 }
 
-// Ring kernel (two teams, three buffers, one CTA per SM) for complex128
-// multi-tile passes.  Off by default: measured on B200 it hides the load
-// latency but ran the 28q gradient 5% slower than two independent CTAs per SM
-// (45.3 s vs 43.0 s); QV_RING=1 selects it for experiments.
-#ifndef QV_RING
-#define QV_RING 0
-#endif
+// TMA pass kernel: stages in flight per CTA (one CTA per SM).  complex128
+// tiles are 64 KiB (3 stages), complex64 tiles 32 KiB (5 stages).
 template <typename T>
-constexpr bool use_ring() { return QV_RING && sizeof(T) == 8 && multi_tile_tb<T>() == 8; }
+constexpr int tma_stages() { return sizeof(T) == 8 ? 3 : 5; }
+typedef void (*TmaFn)(const CUtensorMap, const PassDesc, const TmaArgs, const GroupDesc*, const LaunchEntry*, int,
+                      int64_t);
 template <typename T>
-PassFn<T> ring_kernel(bool pair) {
-    return pair ? &ring_pass_kernel<T, 2> : &ring_pass_kernel<T, 1>;
-}
+TmaFn tma_kernel() { return &tma_pass_kernel<T, tma_stages<T>()>; }
+constexpr size_t kTmaSmemCap = 227 * 1024;
 
 template <typename T>
 void set_kernel_attributes() {
     for (auto fn : pass_kernels<T>())
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    for (bool pair : {false, true}) {
+    for (bool pair : {false, true})
         CK(cudaFuncSetAttribute(pass_kernel_multi<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        if (use_ring<T>())
-            CK(cudaFuncSetAttribute(ring_kernel<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    }
+    CK(cudaFuncSetAttribute(tma_kernel<T>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemCap));
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, []() {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// The state slots of a run (trunk / Psi0 / work states): one allocation, so
+// one tensor map per pass covers every state of a launch.
+struct StateArena {
+    const unsigned char* base = nullptr;
+    uint64_t state_bytes = 0;
+    int64_t slots = 0;
+};
+
+// QVB200_TMA=0 disables the TMA kernel (A/B measurements; the arithmetic, and
+// so every result, is the same either way).
+bool tma_enabled() {
+    static const bool on = !(getenv("QVB200_TMA") && std::string(getenv("QVB200_TMA")) == "0");
+    return on;
 }
 
 template <typename T>
 void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const LaunchEntry* d_ent, int nstates,
-                 int64_t ntiles, const EpiArgs& ep, bool generated) {
+                 int64_t ntiles, const EpiArgs& ep, bool generated, const TmaLayout* tl = nullptr,
+                 const StateArena* arena = nullptr) {
     typedef typename Cx<T>::V V;
     const int tb = pd.k - reg_bits(sizeof(T) == 8 ? 0 : 1);
     const bool multi = ntiles > 1 && tb == multi_tile_tb<T>();
-    const bool ring = multi && use_ring<T>();
-    const bool db = multi && !ring && multi_tile_db<T>();
-    const size_t smem = ring ? (sizeof(V) << pd.k) * 3 + 48 + 16 * sizeof(double) + 8192 + 2 * sizeof(LaunchEntry) +
-                                   (size_t)pd.ng * sizeof(GroupDesc) +
-                                   (size_t)pd.nm * 8 * sizeof(V)
-                             : (sizeof(V) << pd.k) * (db ? 2 : 1) + (size_t)pd.ng * sizeof(GroupDesc) +
-                                   (size_t)pd.nm * 4 * sizeof(V) + 32 * sizeof(double) + (multi ? 8192 : 0);
-    const int threads = ring ? 512 : pass_threads(tb);
-    PassFn<T> fn = ring    ? ring_kernel<T>((ep.flags & F_PAIR) != 0)
-                   : multi ? pass_kernel_multi<T>((ep.flags & F_PAIR) != 0)
-                           : pass_kernels<T>()[tb];
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E.device));
+    cudaEvent_t e0 = E.next_event(), e1 = E.next_event();
+    // ---- TMA kernel: pure store passes of multi-tile states -----------------
+    const size_t tile_bytes = sizeof(V) << pd.k;
+    const size_t mat_bytes = (size_t)pd.nm * 4 * sizeof(V);
+    constexpr int ST = tma_stages<T>();
+    const size_t tma_smem = ST * (tile_bytes + kTmaMatBytes) + 16 * ST + (size_t)pd.ng * sizeof(GroupDesc);
+    if (tl && tl->ok && arena && arena->base && multi && tb == 8 && ep.flags == F_STORE && pd.fresh == 0 &&
+        !generated && pd.ng >= 1 && mat_bytes <= (size_t)kTmaMatBytes && tma_smem <= kTmaSmemCap && tma_enabled() &&
+        encode_tiled()) {
+        TmaArgs ta;
+        std::memset(&ta, 0, sizeof(ta));
+        ta.ndim = tl->ndim;
+        const int elems0 = sizeof(V) / 8;   // 8-byte tensor elements per amplitude
+        cuuint64_t gdim[5], gstride[4];
+        cuuint32_t box[5], estride[5] = {1, 1, 1, 1, 1};
+        for (int d = 0; d < tl->ndim; ++d) {
+            ta.lo[d] = tl->lo[d];
+            ta.cmask[d] = (uint32_t)((1ull << tl->span[d]) - 1);
+            gdim[d] = (cuuint64_t)1 << tl->span[d];
+            box[d] = 1u << tl->box[d];
+            if (d > 0) gstride[d - 1] = ((cuuint64_t)sizeof(V)) << tl->lo[d];
+        }
+        gdim[0] *= elems0;
+        box[0] *= elems0;
+        ta.elems0 = elems0;
+        gdim[tl->ndim] = (cuuint64_t)arena->slots;
+        box[tl->ndim] = 1;
+        gstride[tl->ndim - 1] = arena->state_bytes;
+        for (int d = tl->ndim + 1; d < 5; ++d) {
+            gdim[d] = 1;
+            box[d] = 1;
+            gstride[d - 1] = arena->state_bytes * (cuuint64_t)arena->slots;
+        }
+        CUtensorMap tmap;
+        const CUresult rc = encode_tiled()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, (void*)arena->base, gdim, gstride,
+                                           box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (rc != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)rc) + ")");
+        for (int j = 0; j < 16; ++j) ta.wcombo[j] = tl->wcombo[j];
+        for (int m = 0; m < 8; ++m) ta.wtcol[m] = tl->wtcol[m];
+        ta.base = arena->base;
+        ta.state_bytes = arena->state_bytes;
+        ta.tile_bytes = (uint32_t)tile_bytes;
+        ta.mat_bytes = (uint32_t)mat_bytes;
+        const int64_t items = ntiles * nstates;
+        if (items >= (1ll << 31)) throw ArgError("launch has too many (state, tile) items");
+        const int64_t blocks = std::min<int64_t>(items, sms);
+        CK(cudaEventRecord(e0, E.stream));
+        tma_kernel<T>()<<<(unsigned)blocks, kTmaThreads, tma_smem, E.stream>>>(tmap, pd, ta, d_groups, d_ent, nstates,
+                                                                               ntiles);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(e1, E.stream));
+        E.timed.push_back({e0, e1});
+        E.stats[0] += 1;
+        E.stats[12] += 1;
+        E.stats[11] += (double)nstates * (double)ntiles * (double)(1ll << pd.k) * 14.0 * pd.nm;
+        return;
+    }
+    // ---- pass_kernel ---------------------------------------------------------
+    const size_t smem = tile_bytes + (size_t)pd.ng * sizeof(GroupDesc) + (size_t)pd.nm * 4 * sizeof(V) +
+                        32 * sizeof(double) + (multi ? 8192 : 0);
+    const int threads = pass_threads(tb);
+    PassFn<T> fn = multi ? pass_kernel_multi<T>((ep.flags & F_PAIR) != 0) : pass_kernels<T>()[tb];
     // persistent CTAs: enough per state to fill every SM at full occupancy
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
-    // QVB200_CTAS_PER_SM caps the persistent grid (experiments with several
-    // engines sharing one GPU)
-    static const int cap = getenv("QVB200_CTAS_PER_SM") ? atoi(getenv("QVB200_CTAS_PER_SM")) : 0;
-    if (cap > 0) per_sm = std::min(per_sm, cap);
     per_sm = std::max(per_sm, 1);
-    int sms = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E.device));
     const int64_t slots = (int64_t)per_sm * sms;
     const int64_t blocks = std::min<int64_t>(ntiles * nstates, slots);   // exactly one persistent wave
     if (ntiles * nstates + 4 * blocks >= (1ll << 31)) throw ArgError("launch has too many (state, tile) items");
     EpiArgs e2 = ep;
     e2.ntiles = ntiles;
-    e2.trace = nullptr;
-#ifdef QV_TRACE
-    // debug builds: record a per-phase clock64() timeline of CTA 0 for the
-    // first launch with >= 8 items per CTA; written to $QVB200_TRACE_OUT
-    static bool traced = false;
-    long long* d_trace = nullptr;
-    const char* min_m0 = getenv("QVB200_TRACE_MIN_M0");   // trace a later pass (matrix slot >= value)
-    const bool do_trace = !traced && pd.m0 > 0 && pd.m0 >= (min_m0 ? atoi(min_m0) : 0) &&
-                          ntiles * nstates >= 8 * blocks && getenv("QVB200_TRACE_OUT");
-    if (do_trace) {
-        CK(cudaMalloc(&d_trace, 8 * 64 * 16 * sizeof(long long)));
-        CK(cudaMemsetAsync(d_trace, 0, 8 * 64 * 16 * sizeof(long long), E.stream));
-        e2.trace = d_trace;
-    }
-#endif
-    cudaEvent_t e0 = E.next_event(), e1 = E.next_event();
     CK(cudaEventRecord(e0, E.stream));
     fn<<<(unsigned)blocks, threads, smem, E.stream>>>(pd, d_groups, d_ent, nstates, 0, e2);
     CK(cudaGetLastError());
-#ifdef QV_TRACE
-    if (do_trace) {
-        std::vector<long long> h(8 * 64 * 16);
-        CK(cudaStreamSynchronize(E.stream));
-        CK(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-        cudaFree(d_trace);
-        traced = true;
-        if (FILE* f = fopen(getenv("QVB200_TRACE_OUT"), "wb")) {
-            const int hdr[4] = {pd.k, pd.ng, pd.nm, threads};
-            fwrite(hdr, sizeof(int), 4, f);
-            fwrite(h.data(), sizeof(long long), h.size(), f);
-            fclose(f);
-        }
-    }
-#endif
     CK(cudaEventRecord(e1, E.stream));
     E.timed.push_back({e0, e1});
     E.stats[0] += 1;
@@ -653,6 +684,7 @@ void GroupRun::run() {
         V* trunk = need_trunk ? reinterpret_cast<V*>(base) : nullptr;
         auto work = [&](int64_t b) { return reinterpret_cast<V*>(base + (size_t)((need_trunk ? 1 : 0) + b) * state_bytes); };
         double* partial = E.d_partial.get((size_t)W * ntiles);
+        StateArena arena{base, state_bytes, W + (need_trunk ? 1 : 0)};
 
         // ---- build the whole launch schedule on the host -----------------
         enum LKind { L_PASS, L_FINAL_DIST, L_FULL, L_PAULI };
@@ -752,7 +784,8 @@ void GroupRun::run() {
                 e2.flags = l.flags;
                 e2.partial = partial;
                 if (!(l.flags & F_SUPPORT)) e2.sup_off = nullptr;
-                launch_pass<T>(E, rpd[l.pass], cp.d_groups.p, dent + l.off, l.count, rtiles[l.pass], e2, l.pass == 0);
+                launch_pass<T>(E, rpd[l.pass], cp.d_groups.p, dent + l.off, l.count, rtiles[l.pass], e2, l.pass == 0,
+                               &plan.tma[l.pass], &arena);
                 E.stats[1] += l.count;
                 E.stats[4] += l.bytes;
             } else if (l.kind == L_FINAL_DIST) {
@@ -1042,6 +1075,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     V* trunk = reinterpret_cast<V*>(base_ptr + state_bytes);
     auto work = [&](int64_t b) { return reinterpret_cast<V*>(base_ptr + (size_t)(2 + b) * state_bytes); };
     double* partial = E.d_partial.get((size_t)W * ntiles * 4);
+    StateArena arena{base_ptr, state_bytes, W + 2};
 
     // ---- schedule ----------------------------------------------------------
     struct L { bool pass; int p; size_t off; int count; int flags; double bytes; };
@@ -1093,7 +1127,8 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
             EpiArgs e2 = ep;
             e2.flags = l.flags;
             e2.partial = partial;
-            launch_pass<T>(E, rpd[l.p], cp.d_groups.p, dent + l.off, l.count, rtiles[l.p], e2, l.p == 0);
+            launch_pass<T>(E, rpd[l.p], cp.d_groups.p, dent + l.off, l.count, rtiles[l.p], e2, l.p == 0,
+                           &plan.tma[l.p], &arena);
             E.stats[1] += l.count;
             E.stats[4] += l.bytes;
         } else {
@@ -1268,19 +1303,28 @@ int qv_shift_js(qv_handle h, const qv_circuits* base, int64_t n_shift, const int
     }
 }
 
+// The getters read under the handle's lock (no torn reads while another
+// thread's call rewrites them).  The error text stays valid until the next
+// call on the handle; callers that share a handle between threads serialise
+// call + getters themselves (native.py holds one lock across both).
 const char* qv_last_error(qv_handle h) {
     if (!h) return "null handle";
-    return reinterpret_cast<Engine*>(h)->err.c_str();
+    Engine* E = reinterpret_cast<Engine*>(h);
+    std::lock_guard<std::mutex> lk(E->mu);
+    return E->err.c_str();
 }
 
 int64_t qv_last_error_circuit(qv_handle h) {
     if (!h) return -1;
-    return reinterpret_cast<Engine*>(h)->err_circuit;
+    Engine* E = reinterpret_cast<Engine*>(h);
+    std::lock_guard<std::mutex> lk(E->mu);
+    return E->err_circuit;
 }
 
 int qv_last_stats(qv_handle h, double* stats, int32_t n_stats) {
     if (!h || !stats) return QV_ERR_ARGUMENT;
     Engine* E = reinterpret_cast<Engine*>(h);
+    std::lock_guard<std::mutex> lk(E->mu);
     for (int i = 0; i < n_stats && i < 16; ++i) stats[i] = E->stats[i];
     return QV_OK;
 }

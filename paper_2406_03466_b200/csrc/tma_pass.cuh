@@ -1,0 +1,250 @@
+// tma_pass.cuh — warp-specialised, TMA-fed pass kernel for multi-tile states.
+//
+// One persistent CTA per SM walks the (state, tile) items of one plan pass,
+// state fastest (the same item order as pass_kernel, so co-running CTAs share
+// a trunk tile through L2).  Roles:
+//
+//   warp 8, lane 0  -- producer.  Per item: one cp.async.bulk.tensor load of
+//                      the tile (a box of the <= 5-D tensor view of the state
+//                      batch that the planner chose, TmaLayout) plus a 1-D
+//                      cp.async.bulk of the item's fused matrices into the
+//                      item's stage, both completing on the stage's `full`
+//                      mbarrier; once the compute warps release the stage
+//                      (`done`), one cp.async.bulk.tensor store of the tile
+//                      back to HBM, and after its shared-memory reads retire
+//                      (bulk wait_group.read) the load of item i + STAGES.
+//   warps 0-7       -- compute.  The register groups of pass_kernel (same
+//                      descriptors, same rot2 arithmetic order, so every
+//                      amplitude is bitwise identical to the pass_kernel
+//                      result), named barrier 1 between groups that need it;
+//                      the last group writes in the TMA box layout.
+//
+// The compute warps issue no global loads or stores: HBM streaming is done by
+// the TMA unit behind the FP64 math of the previous / next tiles, which is
+// what the round-1 LDGSTS kernel could not overlap.
+// Replaces, for the bulk of a gradient's passes, the reference's per-gate
+// sweeps (pkg/src/qvirt/kernels.py:18-70).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+
+namespace qvb {
+
+constexpr int kTmaComputeThreads = 256;    // 2^(12 - 4): one register group covers the tile
+constexpr int kTmaThreads = kTmaComputeThreads + 32;
+constexpr int kTmaMatBytes = 4096;         // per-stage matrix area (<= 64 complex128 matrices)
+
+// Per-launch constants of the TMA kernel (passed by value).
+struct TmaArgs {
+    int32_t ndim;             // index dimensions (shared-memory order); dimension ndim = state slot
+    int32_t lo[4];            // lowest global bit of each dimension
+    uint32_t cmask[4];        // coordinate mask of each dimension (span bits)
+    int32_t elems0;           // tensor elements per amplitude in dimension 0 (2 for complex128)
+    uint32_t wcombo[16];      // last group: TMA-layout byte offset of register j
+    uint32_t wtcol[8];        // last group: TMA-layout byte offset of thread bit m
+    const unsigned char* base;   // state-slot array (the tensor's base address)
+    uint64_t state_bytes;
+    uint32_t tile_bytes, mat_bytes;
+};
+
+template <int STAGES>
+struct TmaSmem {   // byte offsets inside dynamic shared memory
+    __host__ __device__ static constexpr uint32_t full(uint32_t tile) { return STAGES * (tile + kTmaMatBytes); }
+    __host__ __device__ static constexpr uint32_t done(uint32_t tile) { return full(tile) + 8 * STAGES; }
+    __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return done(tile) + 8 * STAGES; }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        " WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, const int32_t* c, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+        "l"(tmap), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const void* tmap, const int32_t* c, uint32_t src) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group"
+        " [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(tmap),
+        "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(src)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kTmaComputeThreads) : "memory"); }
+
+template <typename T, int STAGES>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, const TmaArgs ta,
+                const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent, int nstates, int64_t ntiles) {
+    typedef typename Cx<T>::V V;
+    constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
+    constexpr int NA = 1 << R;
+    constexpr int TB = 8;
+    extern __shared__ __align__(1024) unsigned char tma_smem[];
+    unsigned char* smem_raw = tma_smem;
+    const uint32_t TILE = ta.tile_bytes;
+    const uint32_t sbase = smem_u32(smem_raw);
+    GroupDesc* sg = reinterpret_cast<GroupDesc*>(smem_raw + TmaSmem<STAGES>::groups(TILE));
+    const uint32_t full0 = sbase + TmaSmem<STAGES>::full(TILE);
+    const uint32_t done0 = sbase + TmaSmem<STAGES>::done(TILE);
+
+    const int tid = threadIdx.x;
+    const int items = (int)(ntiles * nstates);
+    const int G = gridDim.x;
+    {
+        const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
+        uint4* gdst = reinterpret_cast<uint4*>(sg);
+        for (int i = tid; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
+        if (tid == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(full0 + 8 * s, 1);
+                mbar_init(done0 + 8 * s, kTmaComputeThreads);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            fence_proxy_async_smem();
+        }
+    }
+    __syncthreads();
+    const int my_items = (int)blockIdx.x < items ? (items - 1 - (int)blockIdx.x) / G + 1 : 0;
+
+    if (tid >= kTmaComputeThreads) {
+        // ------------------------------------------------------------ producer
+        if (tid != kTmaComputeThreads) return;
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
+        int32_t oc[STAGES][5];   // store coordinates of the item resident in each stage
+        auto issue_load = [&](int i) {
+            const int w = (int)blockIdx.x + i * G;
+            const int x = w / nstates, y = w - x * nstates;
+            const LaunchEntry e = ent[y];
+            uint64_t o = 0;   // outer offset of tile x (light-cone restricted passes list fewer bits)
+            for (int j = 0; j < pd.n_outer; ++j)
+                if ((x >> j) & 1) o |= 1ull << pd.obits[j];
+            const int s = i % STAGES;
+            int32_t c[5] = {0, 0, 0, 0, 0};
+            for (int d = 0; d < ta.ndim; ++d) c[d] = (int32_t)((o >> ta.lo[d]) & ta.cmask[d]);
+            c[0] *= ta.elems0;
+            c[ta.ndim] = (int32_t)(((const unsigned char*)e.in - ta.base) / ta.state_bytes);
+            const uint32_t bar = full0 + 8 * s;
+            mbar_expect_tx(bar, TILE + ta.mat_bytes);
+            tma_load_5d(sbase + s * TILE, &tmap, c, bar);
+            bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes,
+                      reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4, ta.mat_bytes, bar);
+            for (int d = 0; d < 5; ++d) oc[s][d] = c[d];
+            oc[s][ta.ndim] = (int32_t)(((const unsigned char*)e.out - ta.base) / ta.state_bytes);
+        };
+        for (int i = 0; i < STAGES && i < my_items; ++i) issue_load(i);
+        for (int j = 0; j < my_items; ++j) {
+            const int s = j % STAGES;
+            mbar_wait(done0 + 8 * s, (uint32_t)((j / STAGES) & 1));
+            tma_store_5d(&tmap, oc[s], sbase + s * TILE);
+            bulk_commit();
+            if (j + STAGES < my_items) {
+                bulk_wait_read0();   // the stage's bytes have left shared memory
+                issue_load(j + STAGES);
+            }
+        }
+        bulk_wait0();   // every store has completed before the CTA retires
+        return;
+    }
+
+    // ---------------------------------------------------------------- compute
+    uint32_t wbase = 0;
+#pragma unroll
+    for (int m = 0; m < TB; ++m)
+        if ((tid >> m) & 1) wbase ^= ta.wtcol[m];
+    for (int i = 0; i < my_items; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(full0 + 8 * s, (uint32_t)((i / STAGES) & 1));
+        const V* smat = reinterpret_cast<const V*>(smem_raw + STAGES * TILE + s * kTmaMatBytes);
+        const uint32_t boff = s * TILE;   // a multiple of 2^15 >= every slot offset
+        for (int g = 0; g < pd.ng; ++g) {
+            const GroupDesc& GD = sg[g];
+            const int4 mats = *reinterpret_cast<const int4*>(GD.mat);
+            V m00, m01, m10, m11;
+            if (mats.x >= 0) {
+                const V* M = smat + mats.x * 4;
+                m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
+            }
+            uint32_t base = boff;
+#pragma unroll
+            for (int m = 0; m < TB; ++m)
+                if ((tid >> m) & 1) base ^= GD.tcol[m];
+            uint32_t off[NA];
+#pragma unroll
+            for (int q = 0; q < NA / 4; ++q) {
+                const uint4 c = reinterpret_cast<const uint4*>(GD.combo)[q];
+                off[4 * q] = base ^ c.x;
+                off[4 * q + 1] = base ^ c.y;
+                off[4 * q + 2] = base ^ c.z;
+                off[4 * q + 3] = base ^ c.w;
+            }
+            V a[NA];
+#pragma unroll
+            for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off[j]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
+                if (mi >= 0) {
+                    if (r > 0) {
+                        const V* M = smat + mi * 4;
+                        m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
+                    }
+#pragma unroll
+                    for (int j = 0; j < NA; ++j)
+                        if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
+                }
+            }
+            if (g + 1 < pd.ng) {
+#pragma unroll
+                for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off[j]) = a[j];
+                if (!sg[g + 1].cta_sync) __syncwarp();
+                else compute_sync();
+            } else {
+                // last group: every thread has read its amplitudes before any
+                // is rewritten in the TMA box layout
+                compute_sync();
+#pragma unroll
+                for (int j = 0; j < NA; ++j)
+                    *reinterpret_cast<V*>(smem_raw + (boff ^ wbase ^ ta.wcombo[j])) = a[j];
+            }
+        }
+        fence_proxy_async_smem();   // generic-proxy writes -> visible to the TMA store
+        mbar_arrive(done0 + 8 * s);
+    }
+}
+
+}  // namespace qvb

@@ -32,7 +32,7 @@ EXPORTS = ("qv_version", "qv_output_size", "qv_create", "qv_destroy", "qv_execut
 
 STAT_NAMES = ("launches", "sweeps", "sweeps_unshared", "unique_states", "pass_bytes",
               "pass_ms", "passes_per_circuit", "tile_bits", "device_ms", "h2d_bytes", "d2h_bytes",
-              "pass_flops")
+              "pass_flops", "tma_launches")
 
 
 class NativeUnavailable(RuntimeError):
@@ -118,6 +118,11 @@ class Engine:
         self.last_stats: dict[str, float] = {}
         # running sums over every call (per-call values for the two shape stats)
         self.total_stats: dict[str, float] = dict.fromkeys(STAT_NAMES, 0.0)
+        # Every backend on a device shares this engine (execute_parallel runs
+        # up to V threads on it).  The handle serialises the calls themselves;
+        # this lock also covers reading a call's error text, failing circuit
+        # and stats, so no other thread's call can clear or replace them first.
+        self._call_lock = threading.Lock()
 
     def close(self) -> None:
         if self._handle:
@@ -170,8 +175,9 @@ class Engine:
         if size < 0:
             raise ValueError("malformed result request")
         out = np.empty(max(int(size), 1), dtype=np.float64)
-        code = self._lib.qv_execute(self._handle, ctypes.byref(c), ctypes.byref(r), out.ctypes.data, out.shape[0])
-        self._finish(code)
+        with self._call_lock:
+            code = self._lib.qv_execute(self._handle, ctypes.byref(c), ctypes.byref(r), out.ctypes.data, out.shape[0])
+            self._finish(code)
         return out[:size]
 
     def shift_js(self, n_qubits: int, base: "LoweredBatch", gate_index: np.ndarray, support: np.ndarray,
@@ -193,12 +199,14 @@ class Engine:
         r.support = _ptr(support)
         r.target = _ptr(target)
         out = np.empty(2 * gates.shape[0], dtype=np.float64)
-        code = self._lib.qv_shift_js(self._handle, ctypes.byref(c), gates.shape[0], gates.ctypes.data,
-                                     ctypes.byref(r), out.ctypes.data)
-        self._finish(code)
+        with self._call_lock:
+            code = self._lib.qv_shift_js(self._handle, ctypes.byref(c), gates.shape[0], gates.ctypes.data,
+                                         ctypes.byref(r), out.ctypes.data)
+            self._finish(code)
         return out
 
     def _finish(self, code: int) -> None:
+        """Stats and error of the call just made (caller holds _call_lock)."""
         stats = np.zeros(len(STAT_NAMES), dtype=np.float64)
         self._lib.qv_last_stats(self._handle, stats.ctypes.data, stats.shape[0])
         self.last_stats = dict(zip(STAT_NAMES, stats.tolist()))

@@ -20,6 +20,8 @@ all-gather -- the MPI_Allgatherv of the paper's decorator.
 
 from __future__ import annotations
 
+import contextlib
+import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -27,7 +29,7 @@ from typing import Callable, Sequence
 
 import numpy as np
 
-from .backend import MODES, Accelerator, B200Backend, ExecutionConfig
+from .backend import MODES, Accelerator, B200Backend, ExecutionConfig, ExecutionError
 from .ir import Circuit
 from .results import ChildResult, ResultBuffer, merge
 
@@ -136,7 +138,27 @@ def execute_parallel(buffer: ResultBuffer, circuits: Sequence[Circuit], config: 
 # ---------------------------------------------------------------------------
 # B200 fast path: per-circuit scalars, optionally across torch.distributed ranks
 
+_LOCAL = threading.local()
+
+
+@contextlib.contextmanager
+def rank_local():
+    """Inside this block the scalar fast path ignores torch.distributed and
+    runs every block on this process's GPU, with no collective.  For work a
+    caller has already sharded across ranks (e.g. each rank owns its own data
+    points): without it, every rank would hand the single block of its own
+    batch to rank 0 and receive rank 0's values."""
+    depth = getattr(_LOCAL, "depth", 0)
+    _LOCAL.depth = depth + 1
+    try:
+        yield
+    finally:
+        _LOCAL.depth = depth
+
+
 def _dist_context():
+    if getattr(_LOCAL, "depth", 0):
+        return None
     try:
         import torch.distributed as dist
     except Exception:  # pragma: no cover - torch is part of the image
@@ -202,19 +224,33 @@ def execute_row_values(n_rows: int, config: VqpuPoolConfig, backend_factory: Cal
     mine = [b for i, b in enumerate(blocks) if owner[i] == rank]
     index = np.concatenate([np.arange(b.start, b.end) for b in mine]) if mine else np.zeros(0, np.int64)
     local = np.zeros(0, np.float64)
+    failure: BaseException | None = None
     if mine:
-        backend = backend_factory()
-        local = np.asarray(evaluate_rows(backend, index.astype(np.int64)), dtype=np.float64)
+        try:
+            backend = backend_factory()
+            local = np.asarray(evaluate_rows(backend, index.astype(np.int64)), dtype=np.float64)
+        except Exception as exc:   # reported to every rank through the gather below
+            failure = exc
+            local = np.zeros(0, np.float64)
     per_rank = [sum(b.size for i, b in enumerate(blocks) if owner[i] == r) for r in range(world)]
     width = max(per_rank)
     use_cuda = dist.get_backend() == "nccl"
     device = torch.device("cuda", torch.cuda.current_device()) if use_cuda else torch.device("cpu")
-    send = torch.zeros(width, dtype=torch.float64, device=device)
+    # one extra slot per rank carries its status, so a rank whose blocks
+    # failed still joins the collective and every rank aborts the batch
+    # together (the reference aborts the whole batch, pool.py:96-98)
+    send = torch.zeros(width + 1, dtype=torch.float64, device=device)
     if local.size:
         send[: local.size] = torch.from_numpy(local).to(device)
-    recv = torch.empty(world * width, dtype=torch.float64, device=device)
+    send[width] = 1.0 if failure is not None else 0.0
+    recv = torch.empty(world * (width + 1), dtype=torch.float64, device=device)
     dist.all_gather_into_tensor(recv, send)
-    gathered = recv.cpu().numpy().reshape(world, width)
+    gathered = recv.cpu().numpy().reshape(world, width + 1)
+    failed = [r for r in range(world) if gathered[r, width] != 0.0]
+    if failure is not None:
+        raise failure
+    if failed:
+        raise ExecutionError(f"rank {failed[0]}", f"a block on rank {failed[0]} failed; the batch is aborted")
     values = np.empty(n_rows, np.float64)
     for r in range(world):
         owned = [b for i, b in enumerate(blocks) if owner[i] == r]

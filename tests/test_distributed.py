@@ -120,3 +120,62 @@ def test_execute_row_values_single_process():
     assert values.tolist() == [2.0 * i for i in range(10)]
     with pytest.raises(ValueError):
         qv.execute_row_values(0, qv.VqpuPoolConfig(), StubBackend, lambda b, r: r)
+
+
+def _local_worker(rank, world, port, out):
+    """Ranks with DIFFERENT batches inside vqpu.rank_local(): each runs its own
+    rows on its own device, no collective (bench.py's per-rank data points)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_rows = 5 + 2 * rank
+        with qv.vqpu.rank_local():
+            _, values = qv.execute_row_values(n_rows, qv.VqpuPoolConfig(n_virtual_qpus=1), StubBackend,
+                                              lambda backend, rows: rows * 1.5 + rank)
+        # outside the block the collective path is back
+        _, shared = qv.execute_row_values(4, qv.VqpuPoolConfig(n_virtual_qpus=2), StubBackend,
+                                          lambda backend, rows: rows * 1.0)
+        out[rank] = (values.tolist(), shared.tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_local_rows_per_rank():
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_local_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for rank in range(2):
+        values, shared = out[rank]
+        assert values == [i * 1.5 + rank for i in range(5 + 2 * rank)]
+        assert shared == [0.0, 1.0, 2.0, 3.0]
+
+
+def _failing_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def evaluate_rows(backend, rows):
+            if rank == 1:
+                raise ValueError("device fault on rank 1")
+            return rows * 1.0
+
+        try:
+            qv.execute_row_values(8, qv.VqpuPoolConfig(n_virtual_qpus=2), StubBackend, evaluate_rows)
+            out[rank] = "no error"
+        except qv.ExecutionError as exc:
+            out[rank] = f"ExecutionError: {exc}"
+        except ValueError as exc:
+            out[rank] = f"ValueError: {exc}"
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_failure_on_one_rank_aborts_every_rank():
+    """A rank whose blocks raise still joins the all-gather (status slot), so
+    its peers do not hang in the collective: every rank aborts the batch."""
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_failing_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out[1] == "ValueError: device fault on rank 1"
+    assert out[0].startswith("ExecutionError") and "rank 1" in out[0]

@@ -161,3 +161,65 @@ def test_light_cone_restriction_reads_only_written_data(plan_lib, seed):
     # the low-index support sweeps far fewer tiles than the full passes
     _, visited, passes = _simulate_cone(plan_lib, n, gates, tile, supports[0])
     assert visited < passes * (1 << (n - tile))
+
+
+# ---------------------------------------------------------------------------
+# TMA layouts (tma_pass.cuh): the interpreter loads and stores every pass with
+# a TmaLayout through the TMA box layout computed from the layout's tensor
+# dimensions (independently of the planner's slot columns; a mismatch returns
+# -3), and the last register group writes in that layout.
+
+@pytest.fixture(scope="module")
+def tma_lib(plan_lib):
+    plan_lib.qvp_simulate_tma.restype = ctypes.c_int
+    plan_lib.qvp_simulate_tma.argtypes = plan_lib.qvp_simulate.argtypes
+    plan_lib.qvp_plan_tma.restype = ctypes.c_int
+    plan_lib.qvp_plan_tma.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 3 + [
+        ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int32]
+    return plan_lib
+
+
+def simulate_tma(lib, n, gates, tile_bits, precision=0):
+    kinds, q0, q1, ang = arrays(gates)
+    out = np.zeros(2 << n, np.float64)
+    passes = lib.qvp_simulate_tma(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data,
+                                  ang.ctypes.data, precision, tile_bits, out.ctypes.data)
+    assert passes > 0, passes
+    return out[0::2] + 1j * out[1::2]
+
+
+def tma_layouts(lib, n, gates, tile_bits=0, precision=0):
+    kinds, q0, q1, _ = arrays(gates)
+    out = np.zeros(4 * 128, np.int64)
+    passes = lib.qvp_plan_tma(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data, precision,
+                              tile_bits, out.ctypes.data, 128)
+    assert passes > 0
+    return out[: 4 * passes].reshape(passes, 4)   # ok, ndim, wavefronts, groups
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_tma_layouts_match_oracle(tma_lib, seed):
+    rng = np.random.Generator(np.random.PCG64(100 + seed))
+    n = int(rng.integers(7, 12))
+    gates = sv.random_circuit_gates(rng, n, int(rng.integers(1, 120)), extended=True)
+    want = sv.run_gates(n, gates)
+    for tile, precision in ((5, 0), (6, 0), (8, 0), (7, 1), (8, 1)):
+        got = simulate_tma(tma_lib, n, gates, tile, precision)
+        assert np.max(np.abs(got - want)) < 1e-12, (tile, precision)
+
+
+@pytest.mark.parametrize("n,layers,precision", [(28, 8, 0), (20, 6, 0), (32, 4, 1)])
+def test_qcl_passes_have_tma_layouts(tma_lib, n, layers, precision):
+    """Every pass of the benchmark circuits gets a <= 4-index-dimension TMA
+    layout (plus the state dimension: rank <= 5)."""
+    gates = sv.bind_template(sv.ddcl_template_gates(n, layers), [0.1] * (6 * n * layers))
+    lay = tma_layouts(tma_lib, n, gates, 0, precision)
+    assert (lay[:, 0] == 1).all()
+    assert (lay[:, 1] >= 2).all() and (lay[:, 1] <= 4).all()
+
+
+def test_tma_ddcl_multi_pass(tma_lib):
+    tpl = sv.ddcl_template_gates(12, 3)
+    gates = sv.bind_template(tpl, sv.random_angles(6 * 12 * 3, 9))
+    got = simulate_tma(tma_lib, 12, gates, 8)
+    assert np.max(np.abs(got - sv.run_gates(12, gates))) < 1e-12
