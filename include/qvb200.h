@@ -8,14 +8,14 @@
  * reference would add to `qvirt/backend.py`.
  *
  *   qv_create / qv_destroy   <- one `StatevectorBackend()` instance per
- *                               worker thread (reference pkg/src/qvirt/backend.py:283-295,
+ *                               worker thread (reference pkg/src/qvirt/backend.py:189-201,
  *                               created by `backend_factory()` in pool.py:113-114).
  *   qv_execute               <- `StatevectorBackend.execute(buffer, circuits, config)`
- *                               in expectation mode (backend.py:293-313):
- *                               allocate (:151-157) -> run_gates (:182-185, kernels.py:18-70)
- *                               -> expectation (:188-213, kernels.py:73-87)
- *                               or born_distribution (:216-231, kernels.py:90-94).
- *   qv_last_error*           <- `ExecutionError(circuit_name, message)` (backend.py:130-135):
+ *                               in expectation mode (backend.py:199-219):
+ *                               allocate (:57-63) -> run_gates (:88-91, kernels.py:18-70)
+ *                               -> expectation (:94-119, kernels.py:73-87)
+ *                               or born_distribution (:122-137, kernels.py:90-94).
+ *   qv_last_error*           <- `ExecutionError(circuit_name, message)` (backend.py:36-41):
  *                               the failing circuit index lets the caller raise with the name.
  *
  * Conventions (same as the reference, kernels.py:3-7): qubit 0 is the MOST
@@ -47,22 +47,22 @@ extern "C" {
 #define QV_GATE_CNOT 2      /* q0 = control, q1 = target */
 #define QV_GATE_RY 3
 #define QV_GATE_RZ 4
-#define QV_GATE_MEASURE_ALL 5 /* no-op in exact mode (backend.py:160-179) */
+#define QV_GATE_MEASURE_ALL 5 /* no-op in exact mode (backend.py:66-85) */
 #define QV_GATE_RX 6        /* extension: [[c,-is],[-is,c]]                  */
 #define QV_GATE_CZ 7        /* extension: diag(1,1,1,-1) on (q0,q1)           */
 
 /* ---- amplitude precision -------------------------------------------------- */
-#define QV_COMPLEX128 0     /* the reference's only precision (backend.py:155) */
+#define QV_COMPLEX128 0     /* the reference's only precision (backend.py:61) */
 #define QV_COMPLEX64 1      /* complex64 states, FP64 reductions                */
 
 /* ---- result kinds --------------------------------------------------------- */
 #define QV_OUT_PAULI 0      /* per circuit, per term: <P> (coefficient-free, kernels.py:73-87)  */
-#define QV_OUT_SUPPORT 1    /* per circuit: normalised p on `support` + the norm (backend.py:216-223) */
+#define QV_OUT_SUPPORT 1    /* per circuit: normalised p on `support` + the norm (backend.py:122-129) */
 #define QV_OUT_FULL 2       /* per circuit: all 2^n normalised probabilities (n <= 24)          */
 #define QV_OUT_JS 3         /* per circuit: JS(target || p) via the support+remainder identity  */
                             /* (ddcl.py:37-61 over born_distribution)                            */
 #define QV_OUT_COUNTS 4     /* per circuit: `shots` samples of the outcome distribution with the  */
-                            /* reference's sampler (backend.py:234-251): numpy PCG64 doubles,     */
+                            /* reference's sampler (backend.py:140-157): numpy PCG64 doubles,     */
                             /* inverse CDF on the sequential cumsum, side="right" (n <= 24)       */
 
 typedef struct qv_engine* qv_handle;
@@ -93,7 +93,7 @@ typedef struct qv_results {
     int32_t reserved;
     /* QV_OUT_PAULI: circuit c owns terms [term_offsets[c], term_offsets[c+1]);
      * a term is a Pauli product given by qubit-bit masks (bit n-1-q for qubit q),
-     * exactly the (xmask, ymask, zmask) of backend.py:198-213.                 */
+     * exactly the (xmask, ymask, zmask) of backend.py:104-119.                 */
     const int64_t* term_offsets;
     const uint64_t* xmask;
     const uint64_t* ymask;
@@ -126,8 +126,9 @@ typedef struct qv_results {
 int64_t qv_output_size(const qv_circuits* circuits, const qv_results* results);
 
 /* Create an executor bound to CUDA device `device`.  `memory_budget_bytes`
- * caps the device memory this handle keeps for state vectors (0 = 85% of the
- * device memory that is free at creation). */
+ * caps the device memory this handle keeps for state vectors (0 = whatever it
+ * holds plus 90% of the device memory free at each call, less 1 GiB, so two
+ * handles on one device -- e.g. one per precision -- share it). */
 int qv_create(int device, int precision, uint64_t memory_budget_bytes, qv_handle* out);
 int qv_destroy(qv_handle handle);
 

@@ -28,7 +28,7 @@ def _pair_view(amps: np.ndarray, n: int, q: int) -> np.ndarray:
 
 
 def zero_state(n: int) -> np.ndarray:
-    """|0..0> (backend.py:151-157; the reference caps n at 30)."""
+    """|0..0> (backend.py:57-63; the reference caps n at 30)."""
     a = np.zeros(1 << n, dtype=np.complex128)
     a[0] = 1.0
     return a
@@ -98,7 +98,7 @@ def apply_cz(amps: np.ndarray, n: int, a: int, b: int) -> None:
 
 
 def apply_gate(amps: np.ndarray, n: int, kind: str, targets: Sequence[int], angle: float | None) -> None:
-    """Dispatch of backend.py:160-179 (measure_all is a no-op in exact mode)."""
+    """Dispatch of backend.py:66-85 (measure_all is a no-op in exact mode)."""
     if kind == "h":
         apply_h(amps, n, targets[0])
     elif kind == "x":
@@ -118,7 +118,7 @@ def apply_gate(amps: np.ndarray, n: int, kind: str, targets: Sequence[int], angl
 
 
 def run_gates(n: int, gates: Iterable[tuple[str, Sequence[int], float | None]]) -> np.ndarray:
-    """allocate + run_gates (backend.py:151-185) from (kind, targets, angle) tuples."""
+    """allocate + run_gates (backend.py:57-91) from (kind, targets, angle) tuples."""
     amps = zero_state(n)
     for kind, targets, angle in gates:
         apply_gate(amps, n, kind, targets, angle)
@@ -141,7 +141,7 @@ def pauli_expectation(amps: np.ndarray, n: int, xmask: int, ymask: int, zmask: i
 
 
 def term_masks(factors: Sequence[tuple[int, str]], n: int) -> tuple[int, int, int, int]:
-    """backend.py:198-213: bit 1 << (n-1-q) per factor; returns (x, y, z, ny)."""
+    """backend.py:104-119: bit 1 << (n-1-q) per factor; returns (x, y, z, ny)."""
     m = {"X": 0, "Y": 0, "Z": 0}
     for q, letter in factors:
         m[letter] |= 1 << (n - 1 - q)
@@ -150,7 +150,7 @@ def term_masks(factors: Sequence[tuple[int, str]], n: int) -> tuple[int, int, in
 
 def expectation(amps: np.ndarray, n: int, terms: Sequence[tuple[Sequence[tuple[int, str]], float]],
                 constant: float | None) -> float:
-    """backend.py:188-195: coeff * <P> for one term (constant None), else
+    """backend.py:94-101: coeff * <P> for one term (constant None), else
     constant + sum_i c_i <P_i> in term order."""
     if constant is None:
         (factors, coeff), = terms
@@ -167,7 +167,7 @@ def born_probabilities(amps: np.ndarray) -> np.ndarray:
 
 
 def normalized_probabilities(amps: np.ndarray) -> np.ndarray:
-    """backend.py:216-223: probs / probs.sum()."""
+    """backend.py:122-129: probs / probs.sum()."""
     p = born_probabilities(amps)
     total = p.sum()
     if not total > 0.0:
@@ -176,7 +176,7 @@ def normalized_probabilities(amps: np.ndarray) -> np.ndarray:
 
 
 def born_distribution(amps: np.ndarray, n: int) -> dict[str, float]:
-    """backend.py:226-231: {bitstring: p} for p > 0."""
+    """backend.py:132-137: {bitstring: p} for p > 0."""
     p = normalized_probabilities(amps)
     return {format(i, f"0{n}b"): float(v) for i, v in enumerate(p) if v > 0.0}
 

@@ -1,10 +1,10 @@
 """The accelerator plugin: `B200Backend.execute(buffer, circuits, config)`.
 
-Drop-in for the reference's `StatevectorBackend` (pkg/src/qvirt/backend.py:283-321)
-behind the `Accelerator` protocol (:276-280): one `ChildResult` per circuit in
+Drop-in for the reference's `StatevectorBackend` (pkg/src/qvirt/backend.py:189-227)
+behind the `Accelerator` protocol (:182-186): one `ChildResult` per circuit in
 input order; with an observable the exact expectation (coefficient and
-constant applied as in :188-195), without one the exact outcome distribution
-(:216-231).  Errors name the failing circuit with `ExecutionError` (:130-135)
+constant applied as in :94-101), without one the exact outcome distribution
+(:122-137).  Errors name the failing circuit with `ExecutionError` (:36-41)
 and leave earlier children in the buffer, as the reference's serial loop does.
 
 Everything numerical runs in libqvb200.so on a B200 (native.py).  There is no
@@ -51,7 +51,7 @@ class ExecutionError(RuntimeError):
 
 @dataclass(frozen=True)
 class ExecutionConfig:
-    """How a backend runs one batch (reference backend.py:254-273)."""
+    """How a backend runs one batch (reference backend.py:160-179)."""
 
     mode: str = "expectation"
     shots: int = 8192
@@ -239,7 +239,7 @@ class B200Backend:
     """State-vector executor on one B200.
 
     Instances are cheap; each worker thread of the virtual-QPU pool gets its
-    own (reference backend.py:283-295).  Instances on the same device share
+    own (reference backend.py:189-201).  Instances on the same device share
     one native engine, whose calls serialise.  Without `device`, devices are
     assigned round-robin across the visible GPUs at construction.
     """
@@ -400,7 +400,7 @@ class B200Backend:
 
     @staticmethod
     def _counts_precheck(c, n: int) -> str:
-        """Counts-mode rules of reference backend.py:314-317, pauli.py:147-162."""
+        """Counts-mode rules of reference backend.py:220-223, pauli.py:147-162."""
         obs = c.observable
         if n > MAX_FULL_DISTRIBUTION_QUBITS:
             return f"counts mode samples a 2^{n} distribution; limited to {MAX_FULL_DISTRIBUTION_QUBITS} qubits"
@@ -415,7 +415,7 @@ class B200Backend:
     def _counts_children(self, circuits, n, config: ExecutionConfig) -> list[ChildResult]:
         """Sample `config.shots` outcomes per circuit on the device with the
         reference's sampler: seed = config.seed + first_global_index + offset
-        (backend.py:297, :320), PCG64 doubles, inverse CDF (backend.py:234-251).
+        (backend.py:203, :226), PCG64 doubles, inverse CDF (backend.py:140-157).
         Circuits with a Pauli term are first rotated into its basis (H on each
         X factor; pauli.py:147-162)."""
         from types import SimpleNamespace

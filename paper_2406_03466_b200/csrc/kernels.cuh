@@ -33,6 +33,7 @@ enum EpiFlags : int {
     F_S_FULL = 64,     // single: all normalised probabilities
     F_S_PAULI = 128,   // single: Pauli terms
     F_PAIR = 256,      // multi-tile: shift-pair epilogue over (Psi0 = aux, Xi = this tile)
+    F_MT_PAULI = 512,  // multi-tile: per-tile partial sums of the state's Pauli terms assigned to this sweep
 };
 
 struct LaunchEntry {
@@ -63,6 +64,16 @@ struct EpiArgs {
     const uint64_t* t_phase;
     double* pauli_out;         // [term]
     double* pair_sup;          // F_PAIR: [(rslot * S + pos) * 4 + {|Psi0|^2, |Xi|^2, Im(Psi0 conj Xi), Re(..)}]
+    // F_MT_PAULI: term t of state rslot (term_off) is evaluated by the launch
+    // whose `sweep` equals t_sweep[t]; t_fslot = physical slot offset of the
+    // term's flip mask in that pass's final layout, t_phloc its phase mask in
+    // logical tile bits, t_phout its phase mask on the outer bits
+    int sweep;
+    const int32_t* t_sweep;
+    const uint32_t* t_fslot;
+    const uint32_t* t_phloc;
+    const uint64_t* t_phout;
+    double2* pauli_partial;    // [t * ntiles + tile]
 };
 
 
@@ -96,6 +107,23 @@ __device__ __forceinline__ double block_sum(double v, double* sred) {
     double t = 0.0;
     const int nw = blockDim.x >> 5;
     for (int w = 0; w < nw; ++w) t += sred[w];
+    return t;
+}
+
+// Two deterministic block sums in one pass (8 warps at most per block here).
+__device__ __forceinline__ double2 block_sum2(double a, double b, double* sred) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, off);
+        b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) { sred[2 * warp] = a; sred[2 * warp + 1] = b; }
+    __syncthreads();
+    double2 t = make_double2(0.0, 0.0);
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; ++w) { t.x += sred[2 * w]; t.y += sred[2 * w + 1]; }
     return t;
 }
 
@@ -326,6 +354,36 @@ pass_kernel(const PassDesc pd, const GroupDesc* __restrict__ gdesc, const Launch
             for (int32_t i = lo + tid; i < hi; i += blockDim.x) {
                 const uint32_t slot = apply_cols(pd.fin, K, (uint32_t)ep.sup_local[i]);
                 row[ep.sup_pos[i]] = norm2(*reinterpret_cast<const V*>(tileb + (size_t)slot * sizeof(V)));
+            }
+        }
+        if (MT && PLAIN && (ep.flags & F_MT_PAULI)) {
+            // Pauli terms of this state whose flip bits lie in this pass's
+            // tile: sum_i conj(a[i ^ F]) a[i] (-1)^{|i & PH|} over the tile's
+            // amplitudes (reference kernels.py:73-87), read-only: every term
+            // of the sweep from one pass over the state
+            const int64_t t0 = ep.term_off[e.rslot], t1 = ep.term_off[e.rslot + 1];
+            for (int64_t t = t0; t < t1; ++t) {
+                if (ep.t_sweep[t] != ep.sweep) continue;   // uniform across the block
+                const uint32_t fF = ep.t_fslot[t], PHl = ep.t_phloc[t];
+                double ar = 0.0, ai = 0.0;
+                if (active) {
+#pragma unroll
+                    for (int it = 0; it < NA; ++it) {
+                        const uint32_t l = (uint32_t)tid | ((uint32_t)it << TB);
+                        const uint32_t sl = fslot ^ pd.fin_hi[it];
+                        const V a = *reinterpret_cast<const V*>(tileb + (size_t)sl * sizeof(V));
+                        const V b = *reinterpret_cast<const V*>(tileb + (size_t)(sl ^ fF) * sizeof(V));
+                        const double tr = (double)b.x * (double)a.x + (double)b.y * (double)a.y;
+                        const double ti = (double)b.x * (double)a.y - (double)b.y * (double)a.x;
+                        if (__popc(l & PHl) & 1) { ar -= tr; ai -= ti; }
+                        else { ar += tr; ai += ti; }
+                    }
+                }
+                const double2 sum = block_sum2(ar, ai, sred);
+                if (tid == 0) {
+                    const double sg = (__popcll(outer & ep.t_phout[t]) & 1) ? -1.0 : 1.0;
+                    ep.pauli_partial[t * ntiles + x] = make_double2(sg * sum.x, sg * sum.y);
+                }
             }
         }
         if (PAIR && (ep.flags & F_PAIR)) {
@@ -592,6 +650,27 @@ __global__ void finalize_pauli_kernel(const double2* __restrict__ partial, int64
     if (threadIdx.x == 0) {
         const int q = ny & 3;
         *out = q == 0 ? R : q == 1 ? -I : q == 2 ? -R : I;
+    }
+}
+
+// F_MT_PAULI finalisation: one CTA per term; fixed-order tree over the
+// per-tile partials, then the i^ny factor (kernels.py:87).
+__global__ void finalize_pauli_mt_kernel(const int64_t* __restrict__ terms, int64_t ntiles,
+                                         const double2* __restrict__ partial, const uint64_t* __restrict__ flip,
+                                         const uint64_t* __restrict__ phase, double* __restrict__ out) {
+    __shared__ double sred[32];
+    const int64_t t = terms[blockIdx.x];
+    double ar = 0.0, ai = 0.0;
+    for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) {
+        const double2 p = partial[t * ntiles + i];
+        ar += p.x;
+        ai += p.y;
+    }
+    const double R = block_sum(ar, sred);
+    const double I = block_sum(ai, sred);
+    if (threadIdx.x == 0) {
+        const int ny = __popcll(flip[t] & phase[t]) & 3;   // Y factors both flip and carry phase
+        out[t] = ny == 0 ? R : ny == 1 ? -I : ny == 2 ? -R : I;
     }
 }
 

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <functional>
 #include <stdexcept>
+#include <unordered_map>
 
 namespace qvb {
 
@@ -172,78 +173,176 @@ struct GroupBuilder {
         if (!pending.empty()) pending.back().targets_after |= 1u << t;
     }
 
-    // Order `cand` so its first `beta` entries have linearly independent
-    // shared-memory bank projections under column map `cols` (one wavefront
-    // of lanes is then conflict-free).
-    std::vector<int> bank_order(const std::vector<int>& cand, const uint16_t* cols) const {
-        std::vector<int> order;
-        std::vector<bool> taken(cand.size(), false);
-        const uint32_t bmask = (1u << beta) - 1;
-        uint32_t span = 1u;   // set of bank indices spanned so far ({0})
-        for (size_t i = 0; i < cand.size() && (int)order.size() < beta; ++i) {
-            const uint32_t v = swz(cols[cand[i]]) & bmask;
-            if ((span >> v) & 1u) continue;
-            uint32_t grown = span;
-            for (uint32_t e = 0; e <= bmask; ++e)
-                if ((span >> e) & 1u) grown |= 1u << (e ^ v);
-            span = grown;
-            order.push_back(cand[i]);
-            taken[i] = true;
+    // Shared-memory bank column (16-byte chunk of a 128-byte row for
+    // complex128, 8-byte word for complex64) of pre-swizzle slot column v.
+    uint32_t bank(uint32_t v) const { return swz(v) & ((1u << beta) - 1); }
+    static int rank_gf2(const uint32_t* v, int m) {
+        uint32_t basis[16] = {0};
+        int r = 0;
+        for (int i = 0; i < m; ++i) {
+            uint32_t x = v[i];
+            for (int j = 0; j < r && x; ++j)
+                if ((x ^ basis[j]) < x) x ^= basis[j];
+            if (x) {
+                basis[r++] = x;
+                std::sort(basis, basis + r, [](uint32_t a, uint32_t b) { return a > b; });
+            }
         }
-        for (size_t i = 0; i < cand.size(); ++i)
-            if (!taken[i]) order.push_back(cand[i]);
-        return order;
+        return r;
+    }
+
+    // TMA layout of the pass (init columns) and, at emit time, the inverse of
+    // the final slot map: the last group writes logical fin^-1 in that layout.
+    uint16_t init[16];
+    uint32_t write_bank(uint32_t pre) const {   // pre-swizzle read column -> bank of its TMA write slot
+        const uint32_t logical = qinv[pre];
+        uint32_t t = 0;
+        for (int j = 0; j < k; ++j)
+            if ((logical >> j) & 1u) t ^= init[j];
+        return bank(t);
+    }
+    std::vector<uint32_t> qinv;
+
+    // Best first-`beta` lanes of a group: lanes 0..beta-1 form one shared-
+    // memory wavefront phase, so their bank columns should be independent;
+    // for the last group of a TMA pass the same must hold for the writes in
+    // the TMA layout.  Returns (score, chosen subset bitmask over `lanes`).
+    std::pair<int, uint32_t> lane_choice(const std::vector<int>& lanes, const uint16_t* cols, bool last_tma) const {
+        const int m = (int)lanes.size(), want = std::min(beta, m);
+        std::pair<int, uint32_t> best{-1, 0};
+        for (uint32_t sub = 0; sub < (1u << m); ++sub) {
+            if (__builtin_popcount(sub) != want) continue;
+            uint32_t rv[16], wv[16];
+            int c = 0;
+            for (int i = 0; i < m; ++i)
+                if ((sub >> i) & 1u) {
+                    rv[c] = bank(cols[lanes[i]]);
+                    wv[c] = last_tma ? write_bank(cols[lanes[i]]) : 0;
+                    ++c;
+                }
+            const int score = rank_gf2(rv, c) + (last_tma ? rank_gf2(wv, c) : 0);
+            if (score > best.first) best = {score, sub};
+        }
+        return best;
+    }
+
+    // Register bits of a group (its matrices' bits, padded with bits outside
+    // the warp index) and its lanes, padding chosen for the best lane score.
+    struct Layout { std::vector<int> reg, lanes; uint32_t sub = 0; int score = -1; };
+    Layout group_layout(const Pending& p, uint32_t wmask, bool last_tma) const {
+        uint32_t used = 0;
+        std::vector<int> reg;
+        for (auto& pr : p.ops) { reg.push_back(pr.first); used |= 1u << pr.first; }
+        std::vector<int> cand;
+        for (int b = k - 1; b >= 0; --b)
+            if (!((used >> b) & 1u) && !((wmask >> b) & 1u)) cand.push_back(b);
+        const int need = rbits - (int)reg.size();
+        Layout best;
+        const int m = (int)cand.size();
+        for (uint32_t sub = 0; sub < (1u << m); ++sub) {   // cand is highest-first: ties keep high pads
+            if (__builtin_popcount(sub) != need) continue;
+            Layout l;
+            l.reg = reg;
+            for (int i = 0; i < m; ++i)
+                if ((sub >> i) & 1u) l.reg.push_back(cand[i]);
+            uint32_t u = used;
+            for (int b : l.reg) u |= 1u << b;
+            for (int b = 0; b < k; ++b)
+                if (!((u >> b) & 1u) && !((wmask >> b) & 1u)) l.lanes.push_back(b);
+            auto lc = lane_choice(l.lanes, p.col, last_tma);
+            l.score = lc.first;
+            l.sub = lc.second;
+            if (l.score > best.score) best = l;
+            if (need == 0) break;
+        }
+        return best;
     }
 
     void emit(std::vector<GroupDesc>& out) {
         const int tb = k - rbits;
         const int nwb = tb > 5 ? tb - 5 : 0;           // warp-index bits
         const uint32_t all = (1u << k) - 1;
-        // segments: maximal runs of groups that leave >= nwb bits untouched
-        // (no matrix, no CNOT target in between); those bits index the warp
-        std::vector<uint32_t> wmask(pending.size(), 0);
-        std::vector<int> seg_start(pending.size(), 0);
+        if (tma) {   // inverse of the final slot map Q (col holds it after the last CNOT)
+            qinv.assign((size_t)1 << k, 0);
+            for (uint32_t l = 0; l < (1u << k); ++l) {
+                uint32_t v = 0;
+                for (int j = 0; j < k; ++j)
+                    if ((l >> j) & 1u) v ^= col[j];
+                qinv[v] = l;
+            }
+        }
+        const size_t G = pending.size();
+        std::unordered_map<uint64_t, Layout> memo;   // (group, warp mask) -> layout
+        auto layout_of = [&](size_t g, uint32_t w) -> const Layout& {
+            const uint64_t key = ((uint64_t)g << 32) | w;
+            auto it = memo.find(key);
+            if (it == memo.end()) it = memo.emplace(key, group_layout(pending[g], w, tma && g + 1 == G)).first;
+            return it->second;
+        };
+        // segments: runs of groups that leave >= nwb bits untouched (no
+        // matrix, no CNOT target in between); nwb of those bits index the
+        // warp, so consecutive groups only need __syncwarp.  A segment is
+        // extended only while sharing the warp bits costs no bank conflicts
+        // (a CTA barrier is cheaper than a 2-way conflicted group).
+        auto best_w = [&](size_t s0, size_t e0, uint32_t free_bits) {
+            std::vector<int> fb;
+            for (int b = k - 1; b >= 0; --b)
+                if ((free_bits >> b) & 1u) fb.push_back(b);
+            std::pair<int, uint32_t> best{-1, 0};
+            const int m = (int)fb.size();
+            for (uint32_t sub = 0; sub < (1u << m); ++sub) {   // fb is highest-first: ties keep high bits
+                if (__builtin_popcount(sub) != nwb) continue;
+                uint32_t w = 0;
+                for (int i = 0; i < m; ++i)
+                    if ((sub >> i) & 1u) w |= 1u << fb[i];
+                int score = 0;
+                for (size_t g = s0; g < e0; ++g) score += layout_of(g, w).score;
+                if (score > best.first) best = {score, w};
+            }
+            return best;
+        };
+        auto solo_free = [&](size_t g) {
+            uint32_t f = all;
+            for (auto& pr : pending[g].ops) f &= ~(1u << pr.first);
+            return f;
+        };
+        std::vector<uint32_t> wmask(G, 0);
+        std::vector<int> seg_start(G, 0);
         size_t s = 0;
-        while (s < pending.size()) {
-            uint32_t free_bits = all;
-            for (auto& pr : pending[s].ops) free_bits &= ~(1u << pr.first);
+        while (s < G) {
+            uint32_t free_bits = solo_free(s);
+            auto cur = best_w(s, s + 1, free_bits);
             size_t e = s + 1;
-            while (e < pending.size()) {
+            while (e < G) {
                 uint32_t f = free_bits & ~pending[e - 1].targets_after;
                 for (auto& pr : pending[e].ops) f &= ~(1u << pr.first);
                 if (__builtin_popcount(f) < nwb) break;
+                const auto ext = best_w(s, e + 1, f);
+                const auto solo = best_w(e, e + 1, solo_free(e));
+                if (ext.first < cur.first + solo.first) break;
                 free_bits = f;
+                cur = ext;
                 ++e;
             }
-            uint32_t w = 0;   // the highest free bits become the warp index
-            for (int b = k - 1; b >= 0 && __builtin_popcount(w) < nwb; --b)
-                if ((free_bits >> b) & 1u) w |= 1u << b;
-            for (size_t g = s; g < e; ++g) { wmask[g] = w; seg_start[g] = g == s; }
+            for (size_t g = s; g < e; ++g) { wmask[g] = cur.second; seg_start[g] = g == s; }
             s = e;
         }
-        for (size_t gi = 0; gi < pending.size(); ++gi) {
+        for (size_t gi = 0; gi < G; ++gi) {
             const Pending& p = pending[gi];
             GroupDesc g;
             std::memset(&g, 0, sizeof(g));
-            int reg[kRegBits];
-            uint32_t used = 0;
-            int nr = 0;
+            const Layout l = layout_of(gi, wmask[gi]);
             for (int r = 0; r < kRegBits; ++r) g.mat[r] = -1;
-            for (auto& pr : p.ops) { reg[nr] = pr.first; g.mat[nr] = pr.second; used |= 1u << pr.first; ++nr; }
-            for (int b = k - 1; b >= 0 && nr < rbits; --b)   // pad with bits outside the warp index
-                if (!((used >> b) & 1u) && !((wmask[gi] >> b) & 1u)) { reg[nr] = b; g.mat[nr] = -1; used |= 1u << b; ++nr; }
-            std::vector<int> lanes, warps;
-            for (int b = 0; b < k; ++b) {
-                if ((used >> b) & 1u) continue;
-                if ((wmask[gi] >> b) & 1u) warps.push_back(b);
-                else lanes.push_back(b);
-            }
-            std::vector<int> order = bank_order(lanes, p.col);
-            order.insert(order.end(), warps.begin(), warps.end());
+            for (size_t r = 0; r < p.ops.size(); ++r) g.mat[r] = p.ops[r].second;
+            std::vector<int> order, rest;
+            for (size_t i = 0; i < l.lanes.size(); ++i) ((l.sub >> i) & 1u ? order : rest).push_back(l.lanes[i]);
+            order.insert(order.end(), rest.begin(), rest.end());
+            for (int b = 0; b < k; ++b)
+                if ((wmask[gi] >> b) & 1u) order.push_back(b);
             for (int j = 0; j < (1 << rbits); ++j) {
                 uint32_t sl = 0;
                 for (int r = 0; r < rbits; ++r)
-                    if ((j >> r) & 1) sl ^= swz(p.col[reg[r]]);
+                    if ((j >> r) & 1) sl ^= swz(p.col[l.reg[r]]);
                 g.combo[j] = sl << amp_shift;
             }
             for (size_t m = 0; m < order.size(); ++m) g.tcol[m] = (uint32_t)swz(p.col[order[m]]) << amp_shift;
@@ -337,7 +436,7 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
             gb.rbits = R;
             gb.amp_shift = precision == 0 ? 4 : 3;
             gb.tma = tma;
-            for (int j = 0; j < 16; ++j) gb.col[j] = init_cols[j];
+            for (int j = 0; j < 16; ++j) gb.col[j] = gb.init[j] = init_cols[j];
             for (int j = 0; j < k; ++j) d.swz[j] = gb.phys(j);
             d.g0 = (int)plan.groups.size();
             d.m0 = (int)plan.mat_op.size();
@@ -529,6 +628,7 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
         };
         TmaLayout best_tl;
         uint16_t best_cols[16];
+        int ngroups_of_last = 0;
         int64_t best_wf = -1;
         for (const auto& cand : cands) {
             uint16_t cols[16];
@@ -537,6 +637,7 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
             const size_t g0 = plan.groups.size(), m0 = plan.mat_op.size(), p0 = plan.pdesc.size();
             build_pass(cols, true);
             finish_tma(tl);
+            ngroups_of_last = plan.pdesc.back().ng;
             plan.groups.resize(g0);
             plan.mat_op.resize(m0);
             plan.pdesc.resize(p0);
@@ -545,6 +646,9 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
                 best_tl = tl;
                 std::memcpy(best_cols, cols, sizeof(best_cols));
             }
+            // conflict-free (every access set at 32 lanes / bank columns
+            // wavefronts per register): no candidate can do better
+            if (best_wf >= 0 && best_wf <= (int64_t)ngroups_of_last * 2 * (1 << R) * (32 / rows)) break;
         }
         if (best_wf >= 0) {
             build_pass(best_cols, true);
@@ -682,6 +786,32 @@ PassDesc restrict_pass(const PassDesc& pd, uint64_t free, uint32_t fresh) {
     r.n_outer = m;
     r.fresh = fresh;
     return r;
+}
+
+int tile_low_bits(int precision) { return coalesce_bits(precision); }
+
+PassDesc readonly_pass(const Plan& plan, uint64_t S) {
+    PassDesc d;
+    std::memset(&d, 0, sizeof(d));
+    const int k = plan.k, n = plan.n, R = reg_bits(plan.precision);
+    d.k = k;
+    d.n_outer = n - k;
+    int j = 0, o = 0;
+    for (int b = 0; b < n; ++b) {
+        if ((S >> b) & 1) d.sbits[j++] = (uint8_t)b;
+        else d.obits[o++] = (uint8_t)b;
+    }
+    if (j != k) throw std::runtime_error("read-only pass needs exactly k tile bits");
+    for (int i = 0; i < k; ++i) d.swz[i] = d.fin[i] = (uint16_t)(1u << i);
+    for (int it = 0; it < (1 << R); ++it) {
+        const uint32_t idx = (uint32_t)it << (k - R);
+        d.swz_hi[it] = d.fin_hi[it] = (uint16_t)idx;
+        uint64_t g = 0;
+        for (int i = 0; i < R; ++i)
+            if ((it >> i) & 1) g |= 1ull << d.sbits[k - R + i];
+        d.g_hi[it] = g;
+    }
+    return d;
 }
 
 }  // namespace qvb

@@ -191,6 +191,13 @@ LightCone light_cone(const Plan& plan, const uint64_t* support, int64_t S);
 // The pass restricted to the tiles whose outer bits outside `free` are zero.
 PassDesc restrict_pass(const PassDesc& pd, uint64_t free, uint32_t fresh);
 
+// Low index bits every tile holds (a 128-byte row): 3 for complex128, 4 for complex64.
+int tile_low_bits(int precision);
+
+// A read-only pass (no register groups, identity slot layout) over the tile
+// bit set `S` (k bits, including the low bits): the multi-tile Pauli sweeps.
+PassDesc readonly_pass(const Plan& plan, uint64_t S);
+
 #ifdef __CUDACC__
 #define QV_HD __host__ __device__
 #else

@@ -89,7 +89,7 @@ uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603u
 struct Engine {
     int device = 0;
     int precision = 0;
-    uint64_t budget = 0;
+    uint64_t budget = 0;           // caller's cap on state memory (0: what the device has free)
     cudaStream_t stream = nullptr;
     std::mutex mu;
     std::string err;
@@ -105,7 +105,9 @@ struct Engine {
     DevBuf<double> d_sup_out, d_js_out, d_full_out, d_pauli_out, d_target, d_delta;
     DevBuf<uint64_t> d_support, d_tflip, d_tphase;
     DevBuf<int64_t> d_term_off, d_slots;
-    DevBuf<int32_t> d_sup_off, d_sup_local, d_sup_pos;
+    DevBuf<int32_t> d_sup_off, d_sup_local, d_sup_pos, d_tsweep;
+    DevBuf<uint32_t> d_tfslot, d_tphloc;
+    DevBuf<uint64_t> d_tphout;
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
     // pinned staging for host->device copies: a call's inputs are copied into
@@ -128,7 +130,20 @@ struct Engine {
         pinned_used += need;
         return at;
     }
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;   // pass-kernel (start, stop) of this call
+    struct Timed { cudaEvent_t start, stop; bool tma; double bytes; };
+    std::vector<Timed> timed;   // pass-kernel launches of this call
+
+    // Bytes available for state buffers now: the caller's cap, or this
+    // engine's current state allocation plus 90 % of what the device has
+    // free less 1 GiB for tables (other engines in the process, e.g. the
+    // other precision, have taken their share by then).
+    uint64_t state_budget() {
+        if (budget) return budget;
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const double avail = 0.9 * (double)free_b - (double)(1ull << 30);
+        return d_states.cap + (uint64_t)std::max(0.0, avail);
+    }
 
     size_t amp_bytes() const { return precision == 0 ? 16 : 8; }
     size_t mat_scalar_bytes() const { return precision == 0 ? 8 : 4; }
@@ -330,8 +345,15 @@ template <typename T>
 constexpr int tma_stages() { return sizeof(T) == 8 ? 3 : 5; }
 typedef void (*TmaFn)(const CUtensorMap, const PassDesc, const TmaArgs, const GroupDesc*, const LaunchEntry*, int,
                       int64_t);
+// Compute teams per CTA (QVB200_TMA_TEAMS = 1 or 2, default 2).
+int tma_teams() {
+    static const int t = getenv("QVB200_TMA_TEAMS") ? std::max(1, std::min(2, atoi(getenv("QVB200_TMA_TEAMS")))) : 2;
+    return t;
+}
 template <typename T>
-TmaFn tma_kernel() { return &tma_pass_kernel<T, tma_stages<T>()>; }
+TmaFn tma_kernel(int teams) {
+    return teams == 1 ? &tma_pass_kernel<T, tma_stages<T>(), 1> : &tma_pass_kernel<T, tma_stages<T>(), 2>;
+}
 constexpr size_t kTmaSmemCap = 227 * 1024;
 
 template <typename T>
@@ -340,7 +362,8 @@ void set_kernel_attributes() {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (bool pair : {false, true})
         CK(cudaFuncSetAttribute(pass_kernel_multi<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(tma_kernel<T>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemCap));
+    for (int teams : {1, 2})
+        CK(cudaFuncSetAttribute(tma_kernel<T>(teams), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemCap));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -375,10 +398,12 @@ bool tma_enabled() {
     return on;
 }
 
+// Launches one pass over a batch of states; `bytes` = its algorithmic HBM
+// traffic (stats[4]; stats[14] / [15] = time and bytes of TMA launches).
 template <typename T>
 void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const LaunchEntry* d_ent, int nstates,
                  int64_t ntiles, const EpiArgs& ep, bool generated, const TmaLayout* tl = nullptr,
-                 const StateArena* arena = nullptr) {
+                 const StateArena* arena = nullptr, double bytes = 0.0) {
     typedef typename Cx<T>::V V;
     const int tb = pd.k - reg_bits(sizeof(T) == 8 ? 0 : 1);
     const bool multi = ntiles > 1 && tb == multi_tile_tb<T>();
@@ -432,13 +457,16 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         if (items >= (1ll << 31)) throw ArgError("launch has too many (state, tile) items");
         const int64_t blocks = std::min<int64_t>(items, sms);
         CK(cudaEventRecord(e0, E.stream));
-        tma_kernel<T>()<<<(unsigned)blocks, kTmaThreads, tma_smem, E.stream>>>(tmap, pd, ta, d_groups, d_ent, nstates,
-                                                                               ntiles);
+        const int teams = tma_teams();
+        tma_kernel<T>(teams)<<<(unsigned)blocks, tma_threads(teams), tma_smem, E.stream>>>(tmap, pd, ta, d_groups, d_ent,
+                                                                                           nstates, ntiles);
         CK(cudaGetLastError());
         CK(cudaEventRecord(e1, E.stream));
-        E.timed.push_back({e0, e1});
+        E.timed.push_back({e0, e1, true, bytes});
         E.stats[0] += 1;
+        E.stats[4] += bytes;
         E.stats[12] += 1;
+        E.stats[15] += bytes;
         E.stats[11] += (double)nstates * (double)ntiles * (double)(1ll << pd.k) * 14.0 * pd.nm;
         return;
     }
@@ -460,8 +488,9 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     fn<<<(unsigned)blocks, threads, smem, E.stream>>>(pd, d_groups, d_ent, nstates, 0, e2);
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, E.stream));
-    E.timed.push_back({e0, e1});
+    E.timed.push_back({e0, e1, false, bytes});
     E.stats[0] += 1;
+    E.stats[4] += bytes;
     // algorithmic FP64/FP32 work: 2^(n-1) pairs x 28 flops per fused 2x2
     // matrix (a |0> input only computes tile 0 of a multi-tile state)
     const double amps = generated ? (double)(1ll << pd.k) : (double)ntiles * (double)(1ll << pd.k);
@@ -658,7 +687,98 @@ void GroupRun::run() {
             // support indices outside the reach are never written: zero rows first
             CK(cudaMemsetAsync(ep.sup_out, 0, (size_t)U * (ep.S + 1) * sizeof(double), E.stream));
         }
-        const bool need_state_out = !dist;   // Pauli / full read the stored state
+        // ---- Pauli outputs: every term evaluated read-only inside a pass.
+        // Term t is assigned, from its flip mask alone (so a circuit's values
+        // never depend on its batch), to sweep 0 = the state's last pass when
+        // its flip bits lie in that pass's tile (nothing is stored then), else
+        // to a read-only sweep over the first canonical window of tile bits
+        // (low bits + a run of k - c consecutive bits, windows overlapping by
+        // one bit) that holds its flip bits, else to a sweep of its own bits;
+        // -1 (a per-term pauli_sweep_kernel) only when its flip bits do not
+        // fit one tile.  MC-VQE's nearest-neighbour terms need at most two
+        // sweeps per state instead of one state read per term.
+        const bool pauli = R->kind == QV_OUT_PAULI;
+        std::vector<int32_t> t_sweep;
+        std::vector<uint64_t> sweep_mask;   // sweep s >= 1 -> tile bit set sweep_mask[s - 1]
+        bool need_store_last = !dist;       // the final state is stored for later reads
+        const int64_t NT_all = pauli ? (int64_t)uterm_src.size() : 0;
+        if (pauli && NT_all * ntiles <= ((int64_t)1 << 27)) {
+            const int c = tile_low_bits(E.precision);
+            const uint64_t low = (1ull << c) - 1;
+            uint64_t s_last = 0;
+            for (int b : plan.passes[P - 1].S) s_last |= 1ull << b;
+            auto fill = [&](uint64_t m) {   // pad with the lowest other bits up to k
+                for (int b = 0; b < n && __builtin_popcountll(m) < k; ++b) m |= 1ull << b;
+                return m;
+            };
+            std::vector<uint64_t> windows;
+            for (int start = c; start < n; start += k - c - 1) {
+                uint64_t w = low;
+                for (int b = start; b < std::min(n, start + k - c); ++b) w |= 1ull << b;
+                windows.push_back(fill(w));
+                if (start + k - c >= n) break;
+            }
+            auto sweep_of = [&](uint64_t m) {
+                auto it = std::find(sweep_mask.begin(), sweep_mask.end(), m);
+                if (it != sweep_mask.end()) return (int32_t)(it - sweep_mask.begin()) + 1;
+                sweep_mask.push_back(m);
+                return (int32_t)sweep_mask.size();
+            };
+            t_sweep.assign(NT_all, -1);
+            need_store_last = false;
+            for (int64_t j = 0; j < NT_all; ++j) {
+                const int64_t t = uterm_src[j];
+                const uint64_t F = R->xmask[t] | R->ymask[t];
+                if (!(F & ~s_last)) { t_sweep[j] = 0; continue; }
+                need_store_last = true;
+                int32_t sw = -1;
+                for (uint64_t w : windows)
+                    if (!(F & ~w)) { sw = sweep_of(w); break; }
+                if (sw < 0 && __builtin_popcountll(F | low) <= k) sw = sweep_of(fill(F | low));
+                t_sweep[j] = sw;
+            }
+        }
+        const bool fused_pauli = !t_sweep.empty();
+        const int n_sweeps = (int)sweep_mask.size();
+        for (uint64_t m : sweep_mask) {
+            rpd.push_back(readonly_pass(plan, m));
+            rtiles.push_back(ntiles);
+        }
+        if (fused_pauli) {
+            // per term: flip / phase masks in the tile bits of its sweep's pass
+            std::vector<uint32_t> fslot(NT_all, 0), phloc(NT_all, 0);
+            std::vector<uint64_t> phout(NT_all, 0);
+            for (int64_t j = 0; j < NT_all; ++j) {
+                if (t_sweep[j] < 0) continue;
+                const PassDesc& pd = t_sweep[j] == 0 ? rpd[P - 1] : rpd[P - 1 + t_sweep[j]];
+                const int64_t t = uterm_src[j];
+                const uint64_t F = R->xmask[t] | R->ymask[t], PH = R->ymask[t] | R->zmask[t];
+                uint32_t fl = 0, pl = 0;
+                uint64_t in_tile = 0;
+                for (int q = 0; q < pd.k; ++q) {
+                    in_tile |= 1ull << pd.sbits[q];
+                    if ((F >> pd.sbits[q]) & 1) fl |= 1u << q;
+                    if ((PH >> pd.sbits[q]) & 1) pl |= 1u << q;
+                }
+                fslot[j] = apply_cols(pd.fin, pd.k, fl);
+                phloc[j] = pl;
+                phout[j] = PH & ~in_tile;
+            }
+            int32_t* dsw = E.d_tsweep.get(NT_all);
+            uint32_t* dfs = E.d_tfslot.get(NT_all);
+            uint32_t* dpl = E.d_tphloc.get(NT_all);
+            uint64_t* dpo = E.d_tphout.get(NT_all);
+            h2d(E, dsw, t_sweep.data(), NT_all * 4);
+            h2d(E, dfs, fslot.data(), NT_all * 4);
+            h2d(E, dpl, phloc.data(), NT_all * 4);
+            h2d(E, dpo, phout.data(), NT_all * 8);
+            ep.t_sweep = dsw;
+            ep.t_fslot = dfs;
+            ep.t_phloc = dpl;
+            ep.t_phout = dpo;
+            ep.pauli_partial = E.d_partial2.get((size_t)std::max<int64_t>(1, NT_all * ntiles));
+        }
+        const bool need_state_out = need_store_last;   // full distributions / unfused Pauli terms read the stored state
 
         // pass signatures per unique state
         std::vector<std::vector<uint64_t>> sig(U, std::vector<uint64_t>(P));
@@ -674,7 +794,7 @@ void GroupRun::run() {
 
         // memory: trunk + W work states
         const bool need_trunk = P > 1 && U > 1;
-        const uint64_t avail_states = E.budget / state_bytes;
+        const uint64_t avail_states = E.state_budget() / state_bytes;
         if (avail_states < (need_trunk ? 2u : 1u))
             throw ArgError("a " + std::to_string(n) + "-qubit state (" + std::to_string(state_bytes >> 20) +
                            " MiB) does not fit the memory budget");
@@ -687,7 +807,7 @@ void GroupRun::run() {
         StateArena arena{base, state_bytes, W + (need_trunk ? 1 : 0)};
 
         // ---- build the whole launch schedule on the host -----------------
-        enum LKind { L_PASS, L_FINAL_DIST, L_FULL, L_PAULI };
+        enum LKind { L_PASS, L_FINAL_DIST, L_FULL, L_PAULI, L_FINAL_PAULI };
         struct L {
             LKind kind;
             int pass;
@@ -695,7 +815,7 @@ void GroupRun::run() {
             int count;      // states
             int flags;
             V* state;       // L_FULL / L_PAULI
-            int64_t u, j;   // unique id / unique term
+            int64_t u, j;   // unique id / unique term (L_PASS: Pauli sweep id)
             double bytes;
         };
         std::vector<L> sched;
@@ -717,9 +837,28 @@ void GroupRun::run() {
                     int flags = F_STORE;
                     if (lastp && dist) flags = unit_norm ? F_SUPPORT : F_NORM | F_SUPPORT;
                     if (lastp && probs) flags = F_STORE | F_NORM;
-                    const double rd = (pp == p && p == 0) ? 0.0 : 1.0, wr = (flags & F_STORE) ? 1.0 : 0.0;
+                    if (lastp && fused_pauli) flags = F_MT_PAULI | (need_state_out ? F_STORE : 0);
+                    // algorithmic bytes: each state's write, and its read -- except
+                    // that a chain's first pass reads the shared trunk once for
+                    // all nb states (the others hit it in L2)
+                    const double rd = (pp == p && p == 0) ? 0.0 : (pp == p ? 1.0 / nb : 1.0);
+                    const double wr = (flags & F_STORE) ? 1.0 : 0.0;
                     const double frac = (double)rtiles[pp] / (double)ntiles;
                     sched.push_back({L_PASS, pp, off, nb, flags, nullptr, 0, 0, nb * (double)state_bytes * frac * (rd + wr)});
+                }
+                for (int sw = 1; sw <= n_sweeps; ++sw) {   // read-only Pauli sweeps of the stored states
+                    const size_t off = ents.size();
+                    for (int b = 0; b < nb; ++b)
+                        ents.push_back({(const void*)work(b), nullptr, d_mats + (size_t)D[b0 + b] * slots8, D[b0 + b], b, 0});
+                    sched.push_back({L_PASS, P - 1 + sw, off, nb, F_MT_PAULI, nullptr, 0, sw, nb * (double)state_bytes});
+                }
+                if (fused_pauli) {   // every swept term of the batch: fixed-order sum over tiles
+                    const size_t off = slots_tab.size();
+                    int count = 0;
+                    for (int b = 0; b < nb; ++b)
+                        for (int64_t j = term_off_u[D[b0 + b]]; j < term_off_u[D[b0 + b] + 1]; ++j)
+                            if (t_sweep[j] >= 0) { slots_tab.push_back(j); ++count; }
+                    if (count) sched.push_back({L_FINAL_PAULI, 0, off, count, 0, nullptr, 0, 0, 0});
                 }
                 if (dist || probs) {
                     const size_t off = slots_tab.size();
@@ -731,7 +870,7 @@ void GroupRun::run() {
                     for (int b = 0; b < nb; ++b) {
                         const int64_t u = D[b0 + b];
                         for (int64_t j = term_off_u[u]; j < term_off_u[u + 1]; ++j)
-                            sched.push_back({L_PAULI, 0, 0, 1, 0, work(b), u, j, 0});
+                            if (!fused_pauli || t_sweep[j] < 0) sched.push_back({L_PAULI, 0, 0, 1, 0, work(b), u, j, 0});
                     }
                 }
             }
@@ -783,15 +922,21 @@ void GroupRun::run() {
                 EpiArgs e2 = ep;
                 e2.flags = l.flags;
                 e2.partial = partial;
+                e2.sweep = (int)l.j;
                 if (!(l.flags & F_SUPPORT)) e2.sup_off = nullptr;
                 launch_pass<T>(E, rpd[l.pass], cp.d_groups.p, dent + l.off, l.count, rtiles[l.pass], e2, l.pass == 0,
-                               &plan.tma[l.pass], &arena);
+                               l.pass < P ? &plan.tma[l.pass] : nullptr, &arena, l.bytes);
+                if (l.pass >= P) E.stats[13] += l.count;   // read-only Pauli sweeps of whole states
                 E.stats[1] += l.count;
-                E.stats[4] += l.bytes;
             } else if (l.kind == L_FINAL_DIST) {
                 finalize_dist_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, rtiles[P - 1], partial, ep.sup_out,
                                                                      ep.S, ep.target, ep.js_out, R->kind == QV_OUT_JS,
                                                                      unit_norm);
+                CK(cudaGetLastError());
+                E.stats[0] += 1;
+            } else if (l.kind == L_FINAL_PAULI) {
+                finalize_pauli_mt_kernel<<<l.count, 256, 0, E.stream>>>(dslots + l.off, ntiles, ep.pauli_partial,
+                                                                       ep.t_flip, ep.t_phase, ep.pauli_out);
                 CK(cudaGetLastError());
                 E.stats[0] += 1;
             } else if (l.kind == L_FULL) {
@@ -811,6 +956,7 @@ void GroupRun::run() {
                 finalize_pauli_kernel<<<1, 1024, 0, E.stream>>>(p2, nblk, __builtin_popcountll(R->ymask[t]), ep.pauli_out + l.j);
                 CK(cudaGetLastError());
                 E.stats[0] += 2;
+                E.stats[13] += 1;
             }
         }
         if (!alive.empty()) throw std::runtime_error("scheduler left states unfinished");
@@ -958,13 +1104,15 @@ void execute(Engine& E, const qv_circuits* c, const qv_results* r, double* out, 
     }
     // device time of pass kernels (event pairs recorded by launch_pass; the
     // stream was synchronised when the results were copied back)
-    double ms = 0;
-    for (auto& pr : E.timed) {
+    double ms = 0, tma_ms = 0;
+    for (auto& t : E.timed) {
         float x = 0.f;
-        CK(cudaEventElapsedTime(&x, pr.first, pr.second));
+        CK(cudaEventElapsedTime(&x, t.start, t.stop));
         ms += x;
+        if (t.tma) tma_ms += x;
     }
     E.stats[5] = ms;
+    E.stats[14] = tma_ms;
 }
 
 // ---------------------------------------------------------------------------
@@ -1067,7 +1215,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
 
     // memory: Psi0 + trunk + W work states
     const size_t state_bytes = sizeof(V) << n;
-    const uint64_t avail = E.budget / state_bytes;
+    const uint64_t avail = E.state_budget() / state_bytes;
     if (avail < 3) throw ArgError("shift pairs need three " + std::to_string(n) + "-qubit states in the memory budget");
     const int64_t W = std::max<int64_t>(1, std::min<int64_t>({(int64_t)avail - 2, (int64_t)64, nshift}));
     unsigned char* base_ptr = E.d_states.get((size_t)(W + 2) * state_bytes);
@@ -1104,7 +1252,9 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
                     ents.push_back({in, lastp ? nullptr : (void*)work(b), pp == p ? mats_shift(D[b0 + b]) : mats_base(),
                                     D[b0 + b], b, (const void*)psi0});
                 }
-                const double rd = (pp == p && p == 0) ? 0.0 : 1.0;
+                // a chain's first pass reads the shared trunk once for all nb
+                // states; the pair epilogue reads Xi and Psi0 and stores nothing
+                const double rd = (pp == p && p == 0) ? 0.0 : (pp == p ? 1.0 / nb : 1.0);
                 sched.push_back({true, pp, off, nb, lastp ? F_PAIR : F_STORE, nb * frac(pp) * (lastp ? 2.0 : rd + 1.0)});
             }
             const size_t off = slots_tab.size();
@@ -1128,9 +1278,8 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
             e2.flags = l.flags;
             e2.partial = partial;
             launch_pass<T>(E, rpd[l.p], cp.d_groups.p, dent + l.off, l.count, rtiles[l.p], e2, l.p == 0,
-                           &plan.tma[l.p], &arena);
+                           &plan.tma[l.p], &arena, l.bytes);
             E.stats[1] += l.count;
-            E.stats[4] += l.bytes;
         } else {
             finalize_pair_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, rtiles[P - 1], partial, ep.pair_sup,
                                                                  ep.S, ep.target, d_out, unit_norm, d_delta);
@@ -1175,13 +1324,15 @@ void shift_js(Engine& E, const qv_circuits* c, int64_t nshift, const int64_t* ga
     CachedPlan& cp = get_plan(E, std::move(t));
     if (E.precision == 0) run_shift_pairs<double>(E, cp, c->angles + g0, nshift, gates, r, out);
     else run_shift_pairs<float>(E, cp, c->angles + g0, nshift, gates, r, out);
-    double ms = 0;
-    for (auto& pr : E.timed) {
+    double ms = 0, tma_ms = 0;
+    for (auto& t : E.timed) {
         float x = 0.f;
-        CK(cudaEventElapsedTime(&x, pr.first, pr.second));
+        CK(cudaEventElapsedTime(&x, t.start, t.stop));
         ms += x;
+        if (t.tma) tma_ms += x;
     }
     E.stats[5] = ms;
+    E.stats[14] = tma_ms;
 }
 
 }  // namespace qvb
@@ -1217,9 +1368,7 @@ int qv_create(int device, int precision, uint64_t memory_budget_bytes, qv_handle
         E->precision = precision;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
-        size_t free_b = 0, total_b = 0;
-        CK(cudaMemGetInfo(&free_b, &total_b));
-        E->budget = memory_budget_bytes ? memory_budget_bytes : (uint64_t)(0.85 * (double)free_b);
+        E->budget = memory_budget_bytes;
         set_kernel_attributes<double>();
         set_kernel_attributes<float>();
         *out = reinterpret_cast<qv_handle>(E);
@@ -1241,7 +1390,8 @@ int qv_destroy(qv_handle h) {
         E->d_pauli_out.release(); E->d_target.release(); E->d_support.release(); E->d_tflip.release();
         E->d_tphase.release(); E->d_term_off.release(); E->d_slots.release(); E->d_sup_off.release();
         E->d_delta.release();
-        E->d_sup_local.release(); E->d_sup_pos.release();
+        E->d_sup_local.release(); E->d_sup_pos.release(); E->d_tsweep.release(); E->d_tfslot.release();
+        E->d_tphloc.release(); E->d_tphout.release();
         if (E->pinned) cudaFreeHost(E->pinned);
         E->pinned = nullptr;
         for (auto& kv : E->plans) kv.second->d_groups.release();

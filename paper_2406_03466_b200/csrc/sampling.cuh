@@ -1,4 +1,4 @@
-// sampling.cuh — counts mode (reference backend.py:234-251) on the device.
+// sampling.cuh — counts mode (reference backend.py:140-157) on the device.
 //
 // The reference samples with numpy: edges = cumsum(probs) (sequential
 // additions), u = Generator(PCG64(seed)).random(shots), draws =

@@ -35,8 +35,13 @@
 
 namespace qvb {
 
-constexpr int kTmaComputeThreads = 256;    // 2^(12 - 4): one register group covers the tile
-constexpr int kTmaThreads = kTmaComputeThreads + 32;
+constexpr int kTmaTeamThreads = 256;       // 2^(12 - 4): one register group covers the tile
+// One team: 8 compute warps + a producer warp (288 threads).  Two teams: 16
+// compute warps and no producer warp (512 threads, 128 registers each -- a
+// 17th warp would cut every warp's register share, allocated in 4-warp
+// units, to 96); the team that finishes an item issues its store and the
+// load that reuses the stage (see tma_pass_kernel).
+__host__ __device__ constexpr int tma_threads(int teams) { return teams == 1 ? kTmaTeamThreads + 32 : 2 * kTmaTeamThreads; }
 constexpr int kTmaMatBytes = 4096;         // per-stage matrix area (<= 64 complex128 matrices)
 
 // Per-launch constants of the TMA kernel (passed by value).
@@ -104,16 +109,31 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kTmaComputeThreads) : "memory"); }
+__device__ __forceinline__ void team_sync(int team) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "n"(kTmaTeamThreads) : "memory");
+}
 
-template <typename T, int STAGES>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+// TEAMS compute teams of 8 warps each take alternate items (team t: items
+// t, t + TEAMS, ...), so one team's shared-memory round trips and barriers
+// overlap the other team's FP64 math (with a single team the FP64 pipe sat
+// idle through every load / barrier phase: 46 % busy, ncu).
+//
+// Stage protocol: item i lives in stage i % STAGES.  Its tile + matrices
+// arrive on full[stage] (one expect_tx arrival, the TMA transaction bytes).
+// When its compute is done: one bulk-tensor store of the stage, and once the
+// store has read the stage out of shared memory, the load of item i + STAGES
+// into it.  TEAMS = 1: the producer warp does this, signalled by done[stage];
+// TEAMS = 2: an elected thread of the team that computed item i does it right
+// after the team barrier that closes the item.
+template <typename T, int STAGES, int TEAMS>
+__global__ void __launch_bounds__(tma_threads(TEAMS), 1)
 tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, const TmaArgs ta,
                 const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent, int nstates, int64_t ntiles) {
     typedef typename Cx<T>::V V;
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
     constexpr int NA = 1 << R;
     constexpr int TB = 8;
+    constexpr int COMPUTE = TEAMS * kTmaTeamThreads;
     extern __shared__ __align__(1024) unsigned char tma_smem[];
     unsigned char* smem_raw = tma_smem;
     const uint32_t TILE = ta.tile_bytes;
@@ -122,59 +142,65 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     const uint32_t full0 = sbase + TmaSmem<STAGES>::full(TILE);
     const uint32_t done0 = sbase + TmaSmem<STAGES>::done(TILE);
 
-    const int tid = threadIdx.x;
     const int items = (int)(ntiles * nstates);
     const int G = gridDim.x;
+    const int my_items = (int)blockIdx.x < items ? (items - 1 - (int)blockIdx.x) / G + 1 : 0;
+
+    // Load of item i into stage i % STAGES (issuing thread only); returns the
+    // item's store coordinates through `oc` (5 x int32).
+    auto issue_load = [&](int i, int32_t* oc) {
+        const int w = (int)blockIdx.x + i * G;
+        const int x = w / nstates, y = w - x * nstates;
+        const LaunchEntry e = ent[y];
+        uint64_t o = 0;   // outer offset of tile x (light-cone restricted passes list fewer bits)
+        for (int j = 0; j < pd.n_outer; ++j)
+            if ((x >> j) & 1) o |= 1ull << pd.obits[j];
+        const int s = i % STAGES;
+        int32_t c[5] = {0, 0, 0, 0, 0};
+        for (int d = 0; d < ta.ndim; ++d) c[d] = (int32_t)((o >> ta.lo[d]) & ta.cmask[d]);
+        c[0] *= ta.elems0;
+        // the store coordinates first: the expect_tx arrival below releases
+        // them to whichever thread acquires this stage's full barrier
+        for (int d = 0; d < 5; ++d) oc[d] = c[d];
+        oc[ta.ndim] = (int32_t)(((const unsigned char*)e.out - ta.base) / ta.state_bytes);
+        c[ta.ndim] = (int32_t)(((const unsigned char*)e.in - ta.base) / ta.state_bytes);
+        const uint32_t bar = full0 + 8 * s;
+        mbar_expect_tx(bar, TILE + ta.mat_bytes);
+        tma_load_5d(sbase + s * TILE, &tmap, c, bar);
+        bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes, reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4,
+                  ta.mat_bytes, bar);
+    };
+    // store coordinates of the item resident in each stage (written by the
+    // thread that issued its load, read by the thread that stores it)
+    __shared__ int32_t soc[STAGES][5];
     {
         const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
         uint4* gdst = reinterpret_cast<uint4*>(sg);
-        for (int i = tid; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
-        if (tid == 0) {
+        for (int i = threadIdx.x; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
+        if (threadIdx.x == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(full0 + 8 * s, 1);
-                mbar_init(done0 + 8 * s, kTmaComputeThreads);
+                mbar_init(done0 + 8 * s, kTmaTeamThreads);
             }
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             fence_proxy_async_smem();
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
+            for (int i = 0; i < STAGES && i < my_items; ++i) issue_load(i, soc[i]);
         }
     }
     __syncthreads();
-    const int my_items = (int)blockIdx.x < items ? (items - 1 - (int)blockIdx.x) / G + 1 : 0;
 
-    if (tid >= kTmaComputeThreads) {
-        // ------------------------------------------------------------ producer
-        if (tid != kTmaComputeThreads) return;
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
-        int32_t oc[STAGES][5];   // store coordinates of the item resident in each stage
-        auto issue_load = [&](int i) {
-            const int w = (int)blockIdx.x + i * G;
-            const int x = w / nstates, y = w - x * nstates;
-            const LaunchEntry e = ent[y];
-            uint64_t o = 0;   // outer offset of tile x (light-cone restricted passes list fewer bits)
-            for (int j = 0; j < pd.n_outer; ++j)
-                if ((x >> j) & 1) o |= 1ull << pd.obits[j];
-            const int s = i % STAGES;
-            int32_t c[5] = {0, 0, 0, 0, 0};
-            for (int d = 0; d < ta.ndim; ++d) c[d] = (int32_t)((o >> ta.lo[d]) & ta.cmask[d]);
-            c[0] *= ta.elems0;
-            c[ta.ndim] = (int32_t)(((const unsigned char*)e.in - ta.base) / ta.state_bytes);
-            const uint32_t bar = full0 + 8 * s;
-            mbar_expect_tx(bar, TILE + ta.mat_bytes);
-            tma_load_5d(sbase + s * TILE, &tmap, c, bar);
-            bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes,
-                      reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4, ta.mat_bytes, bar);
-            for (int d = 0; d < 5; ++d) oc[s][d] = c[d];
-            oc[s][ta.ndim] = (int32_t)(((const unsigned char*)e.out - ta.base) / ta.state_bytes);
-        };
-        for (int i = 0; i < STAGES && i < my_items; ++i) issue_load(i);
+    if (threadIdx.x >= COMPUTE) {
+        // --------------------------------------------- producer (TEAMS == 1)
+        if (threadIdx.x != COMPUTE) return;
         for (int j = 0; j < my_items; ++j) {
             const int s = j % STAGES;
             mbar_wait(done0 + 8 * s, (uint32_t)((j / STAGES) & 1));
-            tma_store_5d(&tmap, oc[s], sbase + s * TILE);
+            tma_store_5d(&tmap, soc[s], sbase + s * TILE);
             bulk_commit();
             if (j + STAGES < my_items) {
                 bulk_wait_read0();   // the stage's bytes have left shared memory
-                issue_load(j + STAGES);
+                issue_load(j + STAGES, soc[s]);
             }
         }
         bulk_wait0();   // every store has completed before the CTA retires
@@ -182,11 +208,13 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     }
 
     // ---------------------------------------------------------------- compute
+    const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / kTmaTeamThreads);
+    const int tid = (int)(threadIdx.x % kTmaTeamThreads);
     uint32_t wbase = 0;
 #pragma unroll
     for (int m = 0; m < TB; ++m)
         if ((tid >> m) & 1) wbase ^= ta.wtcol[m];
-    for (int i = 0; i < my_items; ++i) {
+    for (int i = team; i < my_items; i += TEAMS) {
         const int s = i % STAGES;
         mbar_wait(full0 + 8 * s, (uint32_t)((i / STAGES) & 1));
         const V* smat = reinterpret_cast<const V*>(smem_raw + STAGES * TILE + s * kTmaMatBytes);
@@ -203,18 +231,16 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
 #pragma unroll
             for (int m = 0; m < TB; ++m)
                 if ((tid >> m) & 1) base ^= GD.tcol[m];
-            uint32_t off[NA];
-#pragma unroll
-            for (int q = 0; q < NA / 4; ++q) {
-                const uint4 c = reinterpret_cast<const uint4*>(GD.combo)[q];
-                off[4 * q] = base ^ c.x;
-                off[4 * q + 1] = base ^ c.y;
-                off[4 * q + 2] = base ^ c.z;
-                off[4 * q + 3] = base ^ c.w;
-            }
+            // slot of register j = base ^ combo[j]; combo is the XOR of the
+            // four register-bit columns combo[1], [2], [4], [8]
+            const uint4 c0 = reinterpret_cast<const uint4*>(GD.combo)[0];
+            const uint32_t rc0 = c0.y, rc1 = c0.z, rc2 = GD.combo[4], rc3 = GD.combo[8];
+            auto off = [&](int j) -> uint32_t {
+                return base ^ ((j & 1) ? rc0 : 0u) ^ ((j & 2) ? rc1 : 0u) ^ ((j & 4) ? rc2 : 0u) ^ ((j & 8) ? rc3 : 0u);
+            };
             V a[NA];
 #pragma unroll
-            for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off[j]);
+            for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off(j));
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
@@ -230,20 +256,35 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             }
             if (g + 1 < pd.ng) {
 #pragma unroll
-                for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off[j]) = a[j];
+                for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off(j)) = a[j];
                 if (!sg[g + 1].cta_sync) __syncwarp();
-                else compute_sync();
+                else team_sync(team);
             } else {
-                // last group: every thread has read its amplitudes before any
-                // is rewritten in the TMA box layout
-                compute_sync();
+                // last group: every thread of the team has read its amplitudes
+                // before any is rewritten in the TMA box layout
+                team_sync(team);
 #pragma unroll
                 for (int j = 0; j < NA; ++j)
                     *reinterpret_cast<V*>(smem_raw + (boff ^ wbase ^ ta.wcombo[j])) = a[j];
             }
         }
         fence_proxy_async_smem();   // generic-proxy writes -> visible to the TMA store
-        mbar_arrive(done0 + 8 * s);
+        if constexpr (TEAMS == 1) {
+            mbar_arrive(done0 + 8 * s);
+        } else {
+            team_sync(team);
+            if (tid == 0) {
+                tma_store_5d(&tmap, soc[s], sbase + s * TILE);
+                bulk_commit();
+                if (i + STAGES < my_items) {
+                    bulk_wait_read0();   // this thread's store has read the stage
+                    issue_load(i + STAGES, soc[s]);
+                }
+            }
+        }
+    }
+    if constexpr (TEAMS > 1) {
+        if (tid == 0) bulk_wait0();   // this team's stores have completed
     }
 }
 

@@ -32,7 +32,7 @@ EXPORTS = ("qv_version", "qv_output_size", "qv_create", "qv_destroy", "qv_execut
 
 STAT_NAMES = ("launches", "sweeps", "sweeps_unshared", "unique_states", "pass_bytes",
               "pass_ms", "passes_per_circuit", "tile_bits", "device_ms", "h2d_bytes", "d2h_bytes",
-              "pass_flops", "tma_launches")
+              "pass_flops", "tma_launches", "pauli_state_reads", "tma_ms", "tma_bytes")
 
 
 class NativeUnavailable(RuntimeError):
@@ -245,6 +245,17 @@ _engines_lock = threading.Lock()
 
 def device_count() -> int:
     return int(load_library().qv_device_count())
+
+
+def release_engine(device: int, precision: str = "complex128") -> None:
+    """Destroy the process-wide engine of (device, precision) and free its
+    device memory (e.g. a 64 GiB complex128 state before a complex64 run on
+    the same GPU).  Backends created earlier must not be used afterwards."""
+    with _engines_lock:
+        eng = _engines.pop((int(device), precision), None)
+    if eng is not None:
+        with eng._call_lock:
+            eng.close()
 
 
 def engine(device: int, precision: str = "complex128") -> Engine:

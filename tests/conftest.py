@@ -34,6 +34,19 @@ def golden_large():
 
 
 @pytest.fixture(scope="session")
+def golden_big():
+    """Benchmark-size goldens made by the reference's own kernels
+    (tests/golden/make_golden_big.py): qcl20 (config 3), qcl28 (config 4),
+    qcl30c5 (config 5's geometry at the reference's 30-qubit cap)."""
+    out = {}
+    for name in ("qcl20", "qcl28", "qcl30c5", "mcvqe16"):
+        path = GOLDEN / f"golden_big_{name}.json"
+        if path.exists():
+            out[name] = json.loads(path.read_text())
+    return out
+
+
+@pytest.fixture(scope="session")
 def gpu():
     """Skip-free GPU gate: a -m gpu test must fail loudly, not skip, when the
     native library or the device is missing."""

@@ -138,7 +138,7 @@ def qcl_gradient_case(n, layers, theta_seed, target_seed):
 
 
 def counts_cases():
-    """Counts mode (backend.py:234-251, 314-321): sampled tallies from the
+    """Counts mode (backend.py:140-157, 220-227): sampled tallies from the
     reference for random circuits (with and without X/Z terms), and the
     counts-mode DDCL / MC-VQE gradients."""
     out = {"circuits": []}

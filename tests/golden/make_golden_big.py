@@ -20,6 +20,7 @@ only tests/golden/golden_big_<case>.json):
         python tests/golden/make_golden_big.py qcl28   # config 4, ~7 x 4 GiB
     ... qcl30c5    # config 5 geometry at the reference's 30-qubit cap
     ... qcl20      # config 3: gradient entries + batch points
+    ... mcvqe16    # MC-VQE at 16 chromophores, every circuit's expectation
 
 Nothing on the GPU box reads /root/reference; tests read the JSON.
 """
@@ -141,6 +142,22 @@ def main():
         out = dict(meta, qcl=qcl_case(30, 4, 1, 2, (0,), threads=3))
     elif which == "qcl28c5":
         out = dict(meta, qcl=qcl_case(28, 4, 1, 2, (0, 335, 671), threads=7))
+    elif which == "mcvqe16":
+        # MC-VQE at 16 chromophores (the paper's Table-1 sizes): every
+        # shifted circuit's expectation (one coefficient-1 AIEM term each,
+        # mcvqe.py:194-247) through the reference's own pool and kernels.
+        from qvirt import (McvqeAnsatzSpec, ResultBuffer, VqpuPoolConfig, aiem_hamiltonian, mcvqe_energy,
+                           mcvqe_gradient, mcvqe_parameter_count, random_aiem_coefficients,
+                           random_cis_amplitudes)
+        n = 16
+        ham = aiem_hamiltonian(random_aiem_coefficients(n, 0))
+        spec = McvqeAnsatzSpec(random_cis_amplitudes(n, 1), random_angles(mcvqe_parameter_count(n), 2))
+        buf = ResultBuffer(n_qubits=n)
+        rep = mcvqe_gradient(ham, spec, VqpuPoolConfig(n_virtual_qpus=4), buffer=buf)
+        out = dict(meta, mcvqe={"n": n, "coeff_seed": 0, "cis_seed": 1, "theta_seed": 2,
+                                "gradient": list(rep.gradient), "energy": mcvqe_energy(ham, spec),
+                                "n_circuits": rep.n_circuit_executions,
+                                "values": [c.expectation for c in buf.children]})
     elif which == "qcl20":
         # config 3: 20q x 6L gradient entries at 10 parameters (theta seed 1,
         # target seed 2 = batch point 0) and the forward JS of batch points

@@ -101,3 +101,27 @@ def test_js_closed_forms():
     assert sv.js_divergence({"0": 1.0}, {"1": 1.0}) == pytest.approx(math.log(2), abs=1e-12)
     want = 0.5 * (math.log(4 / 3) + 0.5 * math.log(2 / 3) + 0.5 * math.log(2))
     assert sv.js_divergence({"0": 1.0}, {"0": 0.5, "1": 0.5}) == pytest.approx(want, abs=1e-12)
+
+
+def test_oracle_against_reference_at_config3_size():
+    """The oracle restatement against the reference's own 20-qubit x 6-layer
+    goldens (tests/golden/make_golden_big.py qcl20): forward JS and the
+    parameter-0 shifted losses (support + remainder form, normalised by the
+    swept sum as backend.py:122-129 does)."""
+    import json
+    from pathlib import Path
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "golden_big_qcl20.json").read_text())
+    case = g["qcl"]
+    n, layers = case["n"], case["layers"]
+    theta = sv.random_angles(6 * n * layers, case["theta_seed"])
+    target = sv.random_target_distribution(n, case["target_seed"])
+    tpl = sv.ddcl_template_gates(n, layers)
+
+    def loss(row):
+        probs = sv.normalized_probabilities(sv.run_gates(n, sv.bind_template(tpl, row)))
+        return sv.js_support_remainder(target, probs)
+
+    assert abs(loss(theta) - case["js"]) < 1e-12
+    rows = sv.shifted_thetas(theta)
+    assert abs(loss(rows[0]) - case["losses"]["k0+"]) < 1e-12
+    assert abs(loss(rows[1]) - case["losses"]["k0-"]) < 1e-12

@@ -57,7 +57,7 @@ def test_pcg64_restatement_and_jump_ahead(seed):
 
 
 def restated_counts(amps, n, shots, seed):
-    """Reference sampler (backend.py:234-251) on the oracle's probabilities."""
+    """Reference sampler (backend.py:140-157) on the oracle's probabilities."""
     probs = sv.normalized_probabilities(amps)
     edges = np.cumsum(probs)
     u = np.asarray(uniforms(seed, 0, shots))
