@@ -51,6 +51,15 @@ WORKLOADS = {
     "ddcl20l10": ("qcl", 20, 10, "complex128", "paper Table 3: DDCL 20 qubits x 10 layers full gradient (2400 circuits)"),
     "ddcl26l10": ("qcl", 26, 10, "complex128", "paper Table 3: DDCL 26 qubits x 10 layers full gradient (3120 circuits)"),
     "mcvqe8": ("mcvqe", 8, 0, "complex128", "config 2: MC-VQE 8-chromophore parameter-shift gradient"),
+    "mcvqe16": ("mcvqe", 16, 0, "complex128", "MC-VQE 16-chromophore parameter-shift gradient (paper Table 1 size)"),
+    # the literal drop-in: the UNMODIFIED reference driver (baseline/_ref
+    # qvirt.ddcl_gradient -> shifted_circuits -> execute_parallel) calling
+    # B200Backend.execute on every shifted circuit -- its own circuit objects,
+    # no shift pairs; host time of the reference driver is inside the step
+    "qcl28dropin": ("qcl_dropin", 28, 8, "complex128",
+                    "config 4 through the unmodified reference ddcl_gradient with B200Backend as backend_factory"),
+    "qcl20dropin": ("qcl_dropin", 20, 6, "complex128",
+                    "config 3 (one point) through the unmodified reference ddcl_gradient with B200Backend"),
 }
 
 
@@ -379,7 +388,20 @@ def main():
 
     kind, n, layers, precision, desc = WORKLOADS[args.workload]
     s = args.seed
-    if kind == "qcl":
+    if kind == "qcl_dropin":
+        if world > 1:
+            raise SystemExit("the reference driver's pool is single-process; run the drop-in leg with --gpus 1")
+        qvirt = _reference_package()
+        theta = qvirt.random_angles(qvirt.ddcl_parameter_count(n, layers), s + 1)
+        target = qvirt.random_target_distribution(n, s + 2)
+        ref_spec = qvirt.DdclSpec(n, layers, theta, target)
+        ref_pool = qvirt.VqpuPoolConfig(n_virtual_qpus=1, mode="expectation")
+
+        def step():
+            return qvirt.ddcl_gradient(ref_spec, ref_pool,
+                                       backend_factory=lambda: qv.B200Backend(device=device, precision=precision,
+                                                                              support=target))
+    elif kind == "qcl":
         theta = qv.random_angles(qv.ddcl_parameter_count(n, layers), s + 1)
         target = qv.random_target_distribution(n, s + 2)
         spec = qv.DdclSpec(n, layers, theta, target)
@@ -521,6 +543,8 @@ def main():
                 "full_gradient_device_s": dev_ms_max / steps / 1e3,
                 "parallelism": f"vqpu{pool.n_virtual_qpus}->gpu{world} (zigzag blocks), NCCL all-gather of losses",
                 "shift_mode": "none (forward pass)" if kind == "qcl_fwd" else
+                "direct (the reference driver's 2N shifted Circuit objects through B200Backend.execute; "
+                "children carry support + remainder distributions)" if kind == "qcl_dropin" else
                 "pair (psi+- = (Psi0 -+ i Xi_k)/sqrt2: one extra state per parameter)"
                 if kind.startswith("qcl") and n > 12 else "direct",
                 "passes_per_circuit": passes, "tile_bits": tile,
@@ -550,7 +574,9 @@ def main():
                     "d2h_bytes_per_step": d2h / steps,
                     "api": {"qcl": "paper_2406_03466_b200.ddcl_gradient(spec, VqpuPoolConfig, B200Backend)",
                             "qcl_fwd": "paper_2406_03466_b200.ddcl_forward_losses(specs, B200Backend)",
-                            "qcl_batch": "paper_2406_03466_b200.ddcl_gradient per data point"}.get(
+                            "qcl_batch": "paper_2406_03466_b200.ddcl_gradient per data point",
+                            "qcl_dropin": "unmodified reference qvirt.ddcl_gradient(spec, VqpuPoolConfig, "
+                                          "backend_factory=lambda: B200Backend(support=target))"}.get(
                                 kind, "paper_2406_03466_b200.mcvqe_gradient(...)")},
             "gpu_launches": int(float(sm[3])),
             "clocks": clocks.summary(),
@@ -588,6 +614,18 @@ def _ncu_traffic(kernel="tma_pass_kernel"):
                 "traffic_launch": launch["what"], "traffic_source": f"profiles/{name}"}
     except Exception:
         return {"traffic": None}
+
+
+def _reference_package():
+    """The unmodified reference (`qvirt`) installed in baseline/_ref."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "qvirt").exists():
+        raise SystemExit("baseline/_ref is not installed (see DESIGN.md section 7)")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba-qvirt")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import qvirt
+    return qvirt
 
 
 def _measured_peaks():

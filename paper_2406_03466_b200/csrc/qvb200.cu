@@ -354,7 +354,7 @@ template <typename T>
 TmaFn tma_kernel(int teams) {
     return teams == 1 ? &tma_pass_kernel<T, tma_stages<T>(), 1> : &tma_pass_kernel<T, tma_stages<T>(), 2>;
 }
-constexpr size_t kTmaSmemCap = 227 * 1024;
+constexpr size_t kTmaSmemCap = 226 * 1024;   // 227 KiB per block less the kernel's static stage table
 
 template <typename T>
 void set_kernel_attributes() {
@@ -414,7 +414,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const size_t tile_bytes = sizeof(V) << pd.k;
     const size_t mat_bytes = (size_t)pd.nm * 4 * sizeof(V);
     constexpr int ST = tma_stages<T>();
-    const size_t tma_smem = ST * (tile_bytes + kTmaMatBytes) + 16 * ST + (size_t)pd.ng * sizeof(GroupDesc);
+    const size_t tma_smem = TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng);
     if (tl && tl->ok && arena && arena->base && multi && tb == 8 && ep.flags == F_STORE && pd.fresh == 0 &&
         !generated && pd.ng >= 1 && mat_bytes <= (size_t)kTmaMatBytes && tma_smem <= kTmaSmemCap && tma_enabled() &&
         encode_tiled()) {

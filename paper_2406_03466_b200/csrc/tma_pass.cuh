@@ -60,9 +60,20 @@ struct TmaArgs {
 template <int STAGES>
 struct TmaSmem {   // byte offsets inside dynamic shared memory
     __host__ __device__ static constexpr uint32_t full(uint32_t tile) { return STAGES * (tile + kTmaMatBytes); }
-    __host__ __device__ static constexpr uint32_t done(uint32_t tile) { return full(tile) + 8 * STAGES; }
+    __host__ __device__ static constexpr uint32_t done(uint32_t tile) { return full(tile) + 16 * STAGES; }
     __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return done(tile) + 8 * STAGES; }
+    __host__ __device__ static constexpr uint32_t bytes(uint32_t tile, int ng) { return groups(tile) + 128u * ng; }
 };
+// Item i's tile lands on full barrier full_of(i) = (stage, (i / STAGES) mod 2)
+// and completes its phase full_parity(i).  Two barriers per stage: the items
+// sharing one barrier are then 2*STAGES apart -- an even distance, so with
+// two teams they all belong to the same team, which consumes them in order;
+// a team can never wait on a barrier two phases ahead (a parity wait would
+// then see the PREVIOUS phase as done and read a stage still being loaded).
+template <int STAGES>
+__device__ __forceinline__ uint32_t full_of(int i) { return (uint32_t)(i % STAGES + STAGES * ((i / STAGES) & 1)); }
+template <int STAGES>
+__device__ __forceinline__ uint32_t full_parity(int i) { return (uint32_t)((i / (2 * STAGES)) & 1); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -164,7 +175,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         for (int d = 0; d < 5; ++d) oc[d] = c[d];
         oc[ta.ndim] = (int32_t)(((const unsigned char*)e.out - ta.base) / ta.state_bytes);
         c[ta.ndim] = (int32_t)(((const unsigned char*)e.in - ta.base) / ta.state_bytes);
-        const uint32_t bar = full0 + 8 * s;
+        const uint32_t bar = full0 + 8 * full_of<STAGES>(i);
         mbar_expect_tx(bar, TILE + ta.mat_bytes);
         tma_load_5d(sbase + s * TILE, &tmap, c, bar);
         bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes, reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4,
@@ -180,6 +191,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         if (threadIdx.x == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(full0 + 8 * s, 1);
+                mbar_init(full0 + 8 * (STAGES + s), 1);
                 mbar_init(done0 + 8 * s, kTmaTeamThreads);
             }
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -216,7 +228,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         if ((tid >> m) & 1) wbase ^= ta.wtcol[m];
     for (int i = team; i < my_items; i += TEAMS) {
         const int s = i % STAGES;
-        mbar_wait(full0 + 8 * s, (uint32_t)((i / STAGES) & 1));
+        mbar_wait(full0 + 8 * full_of<STAGES>(i), full_parity<STAGES>(i));
         const V* smat = reinterpret_cast<const V*>(smem_raw + STAGES * TILE + s * kTmaMatBytes);
         const uint32_t boff = s * TILE;   // a multiple of 2^15 >= every slot offset
         for (int g = 0; g < pd.ng; ++g) {
