@@ -192,35 +192,36 @@ struct GroupBuilder {
     }
 
     // TMA layout of the pass (init columns) and, at emit time, the inverse of
-    // the final slot map: the last group writes logical fin^-1 in that layout.
+    // the final slot map Q: physical pre-swizzle column -> final logical index.
     uint16_t init[16];
-    uint32_t write_bank(uint32_t pre) const {   // pre-swizzle read column -> bank of its TMA write slot
-        const uint32_t logical = qinv[pre];
-        uint32_t t = 0;
-        for (int j = 0; j < k; ++j)
-            if ((logical >> j) & 1u) t ^= init[j];
-        return bank(t);
-    }
     std::vector<uint32_t> qinv;
 
     // Best first-`beta` lanes of a group: lanes 0..beta-1 form one shared-
     // memory wavefront phase, so their bank columns should be independent;
     // for the last group of a TMA pass the same must hold for the writes in
     // the TMA layout.  Returns (score, chosen subset bitmask over `lanes`).
+    // For the last group of a TMA pass the first lanes should also write one
+    // contiguous 128-byte row of the output (its amplitudes go straight to
+    // HBM): their final logical positions are the tile's low bits 0..c-1.
+    int coalesce_bits_ = 3;
     std::pair<int, uint32_t> lane_choice(const std::vector<int>& lanes, const uint16_t* cols, bool last_tma) const {
         const int m = (int)lanes.size(), want = std::min(beta, m);
         std::pair<int, uint32_t> best{-1, 0};
         for (uint32_t sub = 0; sub < (1u << m); ++sub) {
             if (__builtin_popcount(sub) != want) continue;
-            uint32_t rv[16], wv[16];
-            int c = 0;
+            uint32_t rv[16];
+            int c = 0, row = 0;
+            uint32_t seen = 0;
             for (int i = 0; i < m; ++i)
                 if ((sub >> i) & 1u) {
-                    rv[c] = bank(cols[lanes[i]]);
-                    wv[c] = last_tma ? write_bank(cols[lanes[i]]) : 0;
-                    ++c;
+                    rv[c++] = bank(cols[lanes[i]]);
+                    if (last_tma) {
+                        const uint32_t l = qinv[cols[lanes[i]]];
+                        if (l && !(l & (l - 1)) && l < (1u << coalesce_bits_) && !(seen & l)) { seen |= l; ++row; }
+                    }
                 }
-            const int score = rank_gf2(rv, c) + (last_tma ? rank_gf2(wv, c) : 0);
+            // the read banks first, then the write row
+            const int score = 8 * rank_gf2(rv, c) + row;
             if (score > best.first) best = {score, sub};
         }
         return best;
@@ -436,6 +437,7 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
             gb.rbits = R;
             gb.amp_shift = precision == 0 ? 4 : 3;
             gb.tma = tma;
+            gb.coalesce_bits_ = coalesce_bits(precision);
             for (int j = 0; j < 16; ++j) gb.col[j] = gb.init[j] = init_cols[j];
             for (int j = 0; j < k; ++j) d.swz[j] = gb.phys(j);
             d.g0 = (int)plan.groups.size();
@@ -544,7 +546,18 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
                     tl.wcombo[j] = (uint32_t)apply_cols(d.swz, k, inv[G.combo[j] >> shift]) << shift;
                 for (int mm = 0; mm < tbits && mm < 11; ++mm)
                     tl.wtcol[mm] = (uint32_t)apply_cols(d.swz, k, inv[G.tcol[mm] >> shift]) << shift;
-                wf += access_wf(tl.wcombo, tl.wtcol);
+                // global amplitude offsets of the same final positions
+                auto global_of = [&](uint32_t l) {
+                    uint64_t g = 0;
+                    for (int j = 0; j < k; ++j)
+                        if ((l >> j) & 1u) g |= 1ull << d.sbits[j];
+                    return g;
+                };
+                for (int j = 0; j < (1 << R); ++j) tl.gwcombo[j] = global_of(inv[G.combo[j] >> shift]);
+                for (int mm = 0; mm < tbits && mm < 11; ++mm) tl.gwtcol[mm] = global_of(inv[G.tcol[mm] >> shift]);
+                uint32_t row = 0;
+                for (int mm = 0; mm < c && mm < tbits; ++mm) row |= inv[G.tcol[mm] >> shift];
+                tl.coalesced = row == (1u << c) - 1 ? 1 : 0;
             }
             tl.wavefronts = wf;
         };
@@ -648,7 +661,8 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
             }
             // conflict-free (every access set at 32 lanes / bank columns
             // wavefronts per register): no candidate can do better
-            if (best_wf >= 0 && best_wf <= (int64_t)ngroups_of_last * 2 * (1 << R) * (32 / rows)) break;
+            // (every group's load and store, the last group storing to HBM)
+            if (best_wf >= 0 && best_wf <= (int64_t)(2 * ngroups_of_last - 1) * (1 << R) * (32 / rows)) break;
         }
         if (best_wf >= 0) {
             build_pass(best_cols, true);

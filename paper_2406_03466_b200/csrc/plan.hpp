@@ -139,6 +139,11 @@ struct TmaLayout {
     int32_t box[4] = {0, 0, 0, 0};   // tile bits of the dimension (box = 2^box)
     uint32_t wcombo[16] = {0};  // last group: byte offset of register j in the TMA layout
     uint32_t wtcol[11] = {0};   // last group: byte offset of thread bit m in the TMA layout
+    // the same registers' final positions as global amplitude offsets (OR of
+    // 1 << sbits): the last group can store straight from registers to HBM
+    uint64_t gwcombo[16] = {0};
+    uint64_t gwtcol[11] = {0};
+    int32_t coalesced = 0;      // lanes 0..c-1 of the last group write one contiguous 128-byte row
     int64_t wavefronts = 0;     // bank model of the chosen layout (tools / tests)
 };
 

@@ -63,7 +63,8 @@ static uint64_t tma_outer(const TmaLayout& tl, uint64_t outer) {
 // Final state of one circuit after running its plan; out = 2 * 2^n doubles.
 // tma = 1 interprets every pass with a TMA layout as tma_pass_kernel does
 // (load and store through the TMA box layout, the last register group
-// writing in that layout); tma = 0 as pass_kernel does.
+// writing in that layout); tma = 2 the same load, the last group storing
+// straight to the state; tma = 0 as pass_kernel does.
 // Returns the number of passes, -1 on error, -2 on a warp-locality
 // violation, -3 on a TMA layout inconsistency.
 static int simulate_impl(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
@@ -141,14 +142,20 @@ static int simulate_impl(int n, int64_t n_gates, const uint8_t* kinds, const int
                     const bool last_tma = use_tma && g == pd.g0 + pd.ng - 1;
                     for (int tid = 0; tid < nt; ++tid) {
                         uint32_t base = 0, wbase = 0;
+                        uint64_t gbase = 0;
                         for (int m = 0; m < tb; ++m)
-                            if ((tid >> m) & 1) { base ^= G.tcol[m]; wbase ^= tl.wtcol[m]; }
+                            if ((tid >> m) & 1) { base ^= G.tcol[m]; wbase ^= tl.wtcol[m]; gbase ^= tl.gwtcol[m]; }
                         for (int j = 0; j < NA; ++j) {
+                            if (last_tma && tma == 2) {   // straight from registers to the state
+                                st[outer | (gbase ^ tl.gwcombo[j])] = groups_out[tid][j];
+                                continue;
+                            }
                             const uint32_t at = last_tma ? (wbase ^ tl.wcombo[j]) : (base ^ G.combo[j]);
                             tile[at >> sh] = groups_out[tid][j];
                         }
                     }
                 }
+                if (use_tma && tma == 2) continue;   // the last group stored the tile
                 for (int tid = 0; tid < nt; ++tid) {
                     uint32_t fs = 0;
                     uint64_t tg = 0;
@@ -178,6 +185,14 @@ int qvp_simulate(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0
 int qvp_simulate_tma(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
                      const double* angles, int precision, int max_tile_bits, double* out) {
     return simulate_impl(n, n_gates, kinds, q0, q1, angles, precision, max_tile_bits, out, 1);
+}
+
+// As qvp_simulate_tma, but the last register group of a TMA pass stores its
+// registers straight to the state (gwcombo / gwtcol), as tma_pass_kernel's
+// default mode does.
+int qvp_simulate_tma_direct(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                            const double* angles, int precision, int max_tile_bits, double* out) {
+    return simulate_impl(n, n_gates, kinds, q0, q1, angles, precision, max_tile_bits, out, 2);
 }
 
 // TMA layout of every pass: per pass 4 int64 (ok, ndim, wavefronts, ng);

@@ -350,9 +350,17 @@ int tma_teams() {
     static const int t = getenv("QVB200_TMA_TEAMS") ? std::max(1, std::min(2, atoi(getenv("QVB200_TMA_TEAMS")))) : 2;
     return t;
 }
+// The last register group stores straight to HBM (default) or through the
+// TMA box layout and a bulk-tensor store (QVB200_TMA_STORE=1; always with
+// one team).  Same arithmetic, same results.
+bool tma_direct() {
+    static const bool d = !(getenv("QVB200_TMA_STORE") && std::string(getenv("QVB200_TMA_STORE")) == "1");
+    return d;
+}
 template <typename T>
-TmaFn tma_kernel(int teams) {
-    return teams == 1 ? &tma_pass_kernel<T, tma_stages<T>(), 1> : &tma_pass_kernel<T, tma_stages<T>(), 2>;
+TmaFn tma_kernel(int teams, bool direct) {
+    if (teams == 1) return &tma_pass_kernel<T, tma_stages<T>(), 1, false>;
+    return direct ? &tma_pass_kernel<T, tma_stages<T>(), 2, true> : &tma_pass_kernel<T, tma_stages<T>(), 2, false>;
 }
 constexpr size_t kTmaSmemCap = 226 * 1024;   // 227 KiB per block less the kernel's static stage table
 
@@ -363,7 +371,9 @@ void set_kernel_attributes() {
     for (bool pair : {false, true})
         CK(cudaFuncSetAttribute(pass_kernel_multi<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (int teams : {1, 2})
-        CK(cudaFuncSetAttribute(tma_kernel<T>(teams), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemCap));
+        for (bool direct : {false, true})
+            CK(cudaFuncSetAttribute(tma_kernel<T>(teams, direct), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kTmaSmemCap));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -414,7 +424,10 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const size_t tile_bytes = sizeof(V) << pd.k;
     const size_t mat_bytes = (size_t)pd.nm * 4 * sizeof(V);
     constexpr int ST = tma_stages<T>();
-    const size_t tma_smem = TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng);
+    const int teams = tma_teams();
+    const bool direct = teams > 1 && tma_direct();
+    const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
+    const size_t tma_smem = direct ? tmat_off + 4 * mat_bytes : TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng);
     if (tl && tl->ok && arena && arena->base && multi && tb == 8 && ep.flags == F_STORE && pd.fresh == 0 &&
         !generated && pd.ng >= 1 && mat_bytes <= (size_t)kTmaMatBytes && tma_smem <= kTmaSmemCap && tma_enabled() &&
         encode_tiled()) {
@@ -447,8 +460,15 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
                                            box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (rc != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)rc) + ")");
-        for (int j = 0; j < 16; ++j) ta.wcombo[j] = tl->wcombo[j];
-        for (int m = 0; m < 8; ++m) ta.wtcol[m] = tl->wtcol[m];
+        for (int j = 0; j < 16; ++j) {
+            ta.wcombo[j] = tl->wcombo[j];
+            ta.gwcombo[j] = tl->gwcombo[j];
+        }
+        for (int m = 0; m < 8; ++m) {
+            ta.wtcol[m] = tl->wtcol[m];
+            ta.gwtcol[m] = tl->gwtcol[m];
+        }
+        ta.tmat_off = (uint32_t)tmat_off;
         ta.base = arena->base;
         ta.state_bytes = arena->state_bytes;
         ta.tile_bytes = (uint32_t)tile_bytes;
@@ -457,9 +477,8 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         if (items >= (1ll << 31)) throw ArgError("launch has too many (state, tile) items");
         const int64_t blocks = std::min<int64_t>(items, sms);
         CK(cudaEventRecord(e0, E.stream));
-        const int teams = tma_teams();
-        tma_kernel<T>(teams)<<<(unsigned)blocks, tma_threads(teams), tma_smem, E.stream>>>(tmap, pd, ta, d_groups, d_ent,
-                                                                                           nstates, ntiles);
+        tma_kernel<T>(teams, direct)<<<(unsigned)blocks, tma_threads(teams), tma_smem, E.stream>>>(
+            tmap, pd, ta, d_groups, d_ent, nstates, ntiles);
         CK(cudaGetLastError());
         CK(cudaEventRecord(e1, E.stream));
         E.timed.push_back({e0, e1, true, bytes});

@@ -52,16 +52,19 @@ struct TmaArgs {
     int32_t elems0;           // tensor elements per amplitude in dimension 0 (2 for complex128)
     uint32_t wcombo[16];      // last group: TMA-layout byte offset of register j
     uint32_t wtcol[8];        // last group: TMA-layout byte offset of thread bit m
+    uint64_t gwcombo[16];     // last group, direct stores: global amplitude offset of register j
+    uint64_t gwtcol[8];       // last group, direct stores: global amplitude offset of thread bit m
     const unsigned char* base;   // state-slot array (the tensor's base address)
     uint64_t state_bytes;
     uint32_t tile_bytes, mat_bytes;
+    uint32_t tmat_off;        // direct stores: byte offset of the teams' matrix buffers
 };
 
 template <int STAGES>
 struct TmaSmem {   // byte offsets inside dynamic shared memory
     __host__ __device__ static constexpr uint32_t full(uint32_t tile) { return STAGES * (tile + kTmaMatBytes); }
     __host__ __device__ static constexpr uint32_t done(uint32_t tile) { return full(tile) + 16 * STAGES; }
-    __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return done(tile) + 8 * STAGES; }
+    __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return (done(tile) + 8 * STAGES + 127) & ~127u; }
     __host__ __device__ static constexpr uint32_t bytes(uint32_t tile, int ng) { return groups(tile) + 128u * ng; }
 };
 // Item i's tile lands on full barrier full_of(i) = (stage, (i / STAGES) mod 2)
@@ -130,16 +133,26 @@ __device__ __forceinline__ void team_sync(int team) {
 // idle through every load / barrier phase: 46 % busy, ncu).
 //
 // Stage protocol: item i lives in stage i % STAGES.  Its tile + matrices
-// arrive on full[stage] (one expect_tx arrival, the TMA transaction bytes).
-// When its compute is done: one bulk-tensor store of the stage, and once the
-// store has read the stage out of shared memory, the load of item i + STAGES
-// into it.  TEAMS = 1: the producer warp does this, signalled by done[stage];
-// TEAMS = 2: an elected thread of the team that computed item i does it right
-// after the team barrier that closes the item.
-template <typename T, int STAGES, int TEAMS>
+// arrive on full barrier full_of(i) (one expect_tx arrival + the TMA
+// transaction bytes).  Two ways to give the stage back:
+//  * DIRECT (default, TEAMS = 2): at the item's start the team copies the
+//    item's matrices into its own double buffer; the last register group,
+//    once every thread of the team has read its amplitudes, releases the
+//    stage -- an elected thread issues the load of item i + STAGES into it
+//    right away -- and then stores its registers straight to HBM
+//    (st.global.cs, gwcombo / gwtcol: the final positions as global offsets).
+//    With two teams computing on two of the three stages, the third stage's
+//    turnaround (store read-out + next load) was what starved them (11 % of
+//    warp samples waiting on `full`, ncu); this shortens it to the load alone.
+//  * TMA store: the last group writes the tile back in the TMA box layout and
+//    one bulk-tensor store sends it; once the store has read the stage, the
+//    load of item i + STAGES is issued (by the producer warp for TEAMS = 1,
+//    signalled by done[], or by an elected thread of the team for TEAMS = 2).
+template <typename T, int STAGES, int TEAMS, bool DIRECT>
 __global__ void __launch_bounds__(tma_threads(TEAMS), 1)
 tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, const TmaArgs ta,
                 const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent, int nstates, int64_t ntiles) {
+    static_assert(!DIRECT || TEAMS > 1, "direct stores are issued by the teams themselves");
     typedef typename Cx<T>::V V;
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
     constexpr int NA = 1 << R;
@@ -157,9 +170,12 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     const int G = gridDim.x;
     const int my_items = (int)blockIdx.x < items ? (items - 1 - (int)blockIdx.x) / G + 1 : 0;
 
-    // Load of item i into stage i % STAGES (issuing thread only); returns the
-    // item's store coordinates through `oc` (5 x int32).
-    auto issue_load = [&](int i, int32_t* oc) {
+    // per stage: the resident item's store coordinates (TMA store) or its
+    // output base pointer (direct stores); written by the thread that issues
+    // the item's load, before the arrival that releases them with the tile
+    __shared__ int32_t soc[STAGES][5];
+    __shared__ V* sout[STAGES];
+    auto issue_load = [&](int i) {
         const int w = (int)blockIdx.x + i * G;
         const int x = w / nstates, y = w - x * nstates;
         const LaunchEntry e = ent[y];
@@ -170,10 +186,9 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         int32_t c[5] = {0, 0, 0, 0, 0};
         for (int d = 0; d < ta.ndim; ++d) c[d] = (int32_t)((o >> ta.lo[d]) & ta.cmask[d]);
         c[0] *= ta.elems0;
-        // the store coordinates first: the expect_tx arrival below releases
-        // them to whichever thread acquires this stage's full barrier
-        for (int d = 0; d < 5; ++d) oc[d] = c[d];
-        oc[ta.ndim] = (int32_t)(((const unsigned char*)e.out - ta.base) / ta.state_bytes);
+        for (int d = 0; d < 5; ++d) soc[s][d] = c[d];
+        soc[s][ta.ndim] = (int32_t)(((const unsigned char*)e.out - ta.base) / ta.state_bytes);
+        sout[s] = reinterpret_cast<V*>(e.out) + o;
         c[ta.ndim] = (int32_t)(((const unsigned char*)e.in - ta.base) / ta.state_bytes);
         const uint32_t bar = full0 + 8 * full_of<STAGES>(i);
         mbar_expect_tx(bar, TILE + ta.mat_bytes);
@@ -181,9 +196,6 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes, reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4,
                   ta.mat_bytes, bar);
     };
-    // store coordinates of the item resident in each stage (written by the
-    // thread that issued its load, read by the thread that stores it)
-    __shared__ int32_t soc[STAGES][5];
     {
         const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
         uint4* gdst = reinterpret_cast<uint4*>(sg);
@@ -197,7 +209,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             fence_proxy_async_smem();
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
-            for (int i = 0; i < STAGES && i < my_items; ++i) issue_load(i, soc[i]);
+            for (int i = 0; i < STAGES && i < my_items; ++i) issue_load(i);
         }
     }
     __syncthreads();
@@ -212,7 +224,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             bulk_commit();
             if (j + STAGES < my_items) {
                 bulk_wait_read0();   // the stage's bytes have left shared memory
-                issue_load(j + STAGES, soc[s]);
+                issue_load(j + STAGES);
             }
         }
         bulk_wait0();   // every store has completed before the CTA retires
@@ -223,14 +235,29 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / kTmaTeamThreads);
     const int tid = (int)(threadIdx.x % kTmaTeamThreads);
     uint32_t wbase = 0;
+    uint64_t gbase = 0;
 #pragma unroll
     for (int m = 0; m < TB; ++m)
-        if ((tid >> m) & 1) wbase ^= ta.wtcol[m];
+        if ((tid >> m) & 1) {
+            wbase ^= ta.wtcol[m];
+            if constexpr (DIRECT) gbase ^= ta.gwtcol[m];
+        }
     for (int i = team; i < my_items; i += TEAMS) {
         const int s = i % STAGES;
         mbar_wait(full0 + 8 * full_of<STAGES>(i), full_parity<STAGES>(i));
-        const V* smat = reinterpret_cast<const V*>(smem_raw + STAGES * TILE + s * kTmaMatBytes);
         const uint32_t boff = s * TILE;   // a multiple of 2^15 >= every slot offset
+        const V* smat = reinterpret_cast<const V*>(smem_raw + STAGES * TILE + s * kTmaMatBytes);
+        V* __restrict__ out = nullptr;
+        if constexpr (DIRECT) {
+            // the stage is released before the last group's math: its
+            // matrices move to this team's buffer (double-buffered by item,
+            // so a slow warp of the previous item never sees them change)
+            out = sout[s];
+            V* tm = reinterpret_cast<V*>(smem_raw + ta.tmat_off + (size_t)(2 * team + ((i / TEAMS) & 1)) * ta.mat_bytes);
+            for (int q = tid; q < pd.nm * 4; q += kTmaTeamThreads) tm[q] = smat[q];
+            team_sync(team);
+            smat = tm;
+        }
         for (int g = 0; g < pd.ng; ++g) {
             const GroupDesc& GD = sg[g];
             const int4 mats = *reinterpret_cast<const int4*>(GD.mat);
@@ -253,6 +280,13 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             V a[NA];
 #pragma unroll
             for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off(j));
+            const bool last = g + 1 == pd.ng;
+            if (DIRECT && last) {
+                // every thread of the team has read the stage: hand it to the
+                // load of item i + STAGES
+                team_sync(team);
+                if (tid == 0 && i + STAGES < my_items) issue_load(i + STAGES);
+            }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
@@ -266,36 +300,41 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                         if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
                 }
             }
-            if (g + 1 < pd.ng) {
+            if (!last) {
 #pragma unroll
                 for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off(j)) = a[j];
                 if (!sg[g + 1].cta_sync) __syncwarp();
                 else team_sync(team);
+            } else if constexpr (DIRECT) {
+#pragma unroll
+                for (int j = 0; j < NA; ++j) __stcs(out + (gbase ^ ta.gwcombo[j]), a[j]);
             } else {
-                // last group: every thread of the team has read its amplitudes
-                // before any is rewritten in the TMA box layout
+                // every thread of the team has read its amplitudes before any
+                // is rewritten in the TMA box layout
                 team_sync(team);
 #pragma unroll
                 for (int j = 0; j < NA; ++j)
                     *reinterpret_cast<V*>(smem_raw + (boff ^ wbase ^ ta.wcombo[j])) = a[j];
             }
         }
-        fence_proxy_async_smem();   // generic-proxy writes -> visible to the TMA store
-        if constexpr (TEAMS == 1) {
-            mbar_arrive(done0 + 8 * s);
-        } else {
-            team_sync(team);
-            if (tid == 0) {
-                tma_store_5d(&tmap, soc[s], sbase + s * TILE);
-                bulk_commit();
-                if (i + STAGES < my_items) {
-                    bulk_wait_read0();   // this thread's store has read the stage
-                    issue_load(i + STAGES, soc[s]);
+        if constexpr (!DIRECT) {
+            fence_proxy_async_smem();   // generic-proxy writes -> visible to the TMA store
+            if constexpr (TEAMS == 1) {
+                mbar_arrive(done0 + 8 * s);
+            } else {
+                team_sync(team);
+                if (tid == 0) {
+                    tma_store_5d(&tmap, soc[s], sbase + s * TILE);
+                    bulk_commit();
+                    if (i + STAGES < my_items) {
+                        bulk_wait_read0();   // this thread's store has read the stage
+                        issue_load(i + STAGES);
+                    }
                 }
             }
         }
     }
-    if constexpr (TEAMS > 1) {
+    if constexpr (TEAMS > 1 && !DIRECT) {
         if (tid == 0) bulk_wait0();   // this team's stores have completed
     }
 }

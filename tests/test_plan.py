@@ -171,19 +171,23 @@ def test_light_cone_restriction_reads_only_written_data(plan_lib, seed):
 
 @pytest.fixture(scope="module")
 def tma_lib(plan_lib):
-    plan_lib.qvp_simulate_tma.restype = ctypes.c_int
-    plan_lib.qvp_simulate_tma.argtypes = plan_lib.qvp_simulate.argtypes
+    for f in (plan_lib.qvp_simulate_tma, plan_lib.qvp_simulate_tma_direct):
+        f.restype = ctypes.c_int
+        f.argtypes = plan_lib.qvp_simulate.argtypes
     plan_lib.qvp_plan_tma.restype = ctypes.c_int
     plan_lib.qvp_plan_tma.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 3 + [
         ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int32]
     return plan_lib
 
 
-def simulate_tma(lib, n, gates, tile_bits, precision=0):
+def simulate_tma(lib, n, gates, tile_bits, precision=0, direct=False):
+    """direct: the last register group stores straight to the state (the
+    kernel's default); else through the TMA box layout and a TMA store."""
     kinds, q0, q1, ang = arrays(gates)
     out = np.zeros(2 << n, np.float64)
-    passes = lib.qvp_simulate_tma(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data,
-                                  ang.ctypes.data, precision, tile_bits, out.ctypes.data)
+    fn = lib.qvp_simulate_tma_direct if direct else lib.qvp_simulate_tma
+    passes = fn(n, len(gates), kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data,
+                ang.ctypes.data, precision, tile_bits, out.ctypes.data)
     assert passes > 0, passes
     return out[0::2] + 1j * out[1::2]
 
@@ -204,8 +208,9 @@ def test_tma_layouts_match_oracle(tma_lib, seed):
     gates = sv.random_circuit_gates(rng, n, int(rng.integers(1, 120)), extended=True)
     want = sv.run_gates(n, gates)
     for tile, precision in ((5, 0), (6, 0), (8, 0), (7, 1), (8, 1)):
-        got = simulate_tma(tma_lib, n, gates, tile, precision)
-        assert np.max(np.abs(got - want)) < 1e-12, (tile, precision)
+        for direct in (False, True):
+            got = simulate_tma(tma_lib, n, gates, tile, precision, direct)
+            assert np.max(np.abs(got - want)) < 1e-12, (tile, precision, direct)
 
 
 @pytest.mark.parametrize("n,layers,precision", [(28, 8, 0), (20, 6, 0), (32, 4, 1)])
@@ -221,5 +226,6 @@ def test_qcl_passes_have_tma_layouts(tma_lib, n, layers, precision):
 def test_tma_ddcl_multi_pass(tma_lib):
     tpl = sv.ddcl_template_gates(12, 3)
     gates = sv.bind_template(tpl, sv.random_angles(6 * 12 * 3, 9))
-    got = simulate_tma(tma_lib, 12, gates, 8)
-    assert np.max(np.abs(got - sv.run_gates(12, gates))) < 1e-12
+    for direct in (False, True):
+        got = simulate_tma(tma_lib, 12, gates, 8, direct=direct)
+        assert np.max(np.abs(got - sv.run_gates(12, gates))) < 1e-12
