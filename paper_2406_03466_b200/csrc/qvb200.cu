@@ -130,7 +130,13 @@ struct Engine {
         pinned_used += need;
         return at;
     }
-    struct Timed { cudaEvent_t start, stop; bool tma; double bytes; };
+    struct Timed {
+        cudaEvent_t start, stop;
+        bool tma;
+        double bytes;
+        int m0, nm, nstates;   // pass (first matrix slot, matrices) and states of the launch
+        int64_t ntiles;
+    };
     std::vector<Timed> timed;   // pass-kernel launches of this call
 
     // Bytes available for state buffers now: the caller's cap, or this
@@ -350,11 +356,14 @@ int tma_teams() {
     static const int t = getenv("QVB200_TMA_TEAMS") ? std::max(1, std::min(2, atoi(getenv("QVB200_TMA_TEAMS")))) : 2;
     return t;
 }
-// The last register group stores straight to HBM (default) or through the
-// TMA box layout and a bulk-tensor store (QVB200_TMA_STORE=1; always with
-// one team).  Same arithmetic, same results.
+// The last register group writes the tile back in the TMA box layout for one
+// bulk-tensor store (default), or stores its registers straight to HBM
+// (QVB200_TMA_DIRECT=1, two teams).  Same arithmetic, same results.
+// Measured on B200, 28q x 8L gradient: bulk stores 32.9-33.2 s, direct
+// register stores 36.7-36.9 s (the stage turnaround they save costs less
+// than 16 st.global.v2.f64 per thread per tile from the compute warps).
 bool tma_direct() {
-    static const bool d = !(getenv("QVB200_TMA_STORE") && std::string(getenv("QVB200_TMA_STORE")) == "1");
+    static const bool d = getenv("QVB200_TMA_DIRECT") && std::string(getenv("QVB200_TMA_DIRECT")) == "1";
     return d;
 }
 template <typename T>
@@ -408,6 +417,23 @@ bool tma_enabled() {
     return on;
 }
 
+// QVB200_LAUNCH_LOG=<file>: append one line per pass launch of every call
+// (kernel, first matrix slot, matrices, states, tiles, ms, algorithmic bytes)
+// -- the per-pass roofline breakdown in profiles/ comes from this.
+void log_launches(Engine& E) {
+    static const char* path = getenv("QVB200_LAUNCH_LOG");
+    if (!path) return;
+    FILE* f = fopen(path, "a");
+    if (!f) return;
+    for (auto& t : E.timed) {
+        float x = 0.f;
+        cudaEventElapsedTime(&x, t.start, t.stop);
+        fprintf(f, "%s %d %d %d %lld %.6f %.0f\n", t.tma ? "tma" : "pass", t.m0, t.nm, t.nstates,
+                (long long)t.ntiles, x, t.bytes);
+    }
+    fclose(f);
+}
+
 // Launches one pass over a batch of states; `bytes` = its algorithmic HBM
 // traffic (stats[4]; stats[14] / [15] = time and bytes of TMA launches).
 template <typename T>
@@ -427,7 +453,8 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const int teams = tma_teams();
     const bool direct = teams > 1 && tma_direct();
     const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
-    const size_t tma_smem = direct ? tmat_off + 4 * mat_bytes : TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng);
+    const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);
+    const size_t tma_smem = ent_off + (size_t)nstates * 3 * sizeof(uint64_t);
     if (tl && tl->ok && arena && arena->base && multi && tb == 8 && ep.flags == F_STORE && pd.fresh == 0 &&
         !generated && pd.ng >= 1 && mat_bytes <= (size_t)kTmaMatBytes && tma_smem <= kTmaSmemCap && tma_enabled() &&
         encode_tiled()) {
@@ -469,6 +496,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
             ta.gwtcol[m] = tl->gwtcol[m];
         }
         ta.tmat_off = (uint32_t)tmat_off;
+        ta.ent_off = (uint32_t)ent_off;
         ta.base = arena->base;
         ta.state_bytes = arena->state_bytes;
         ta.tile_bytes = (uint32_t)tile_bytes;
@@ -481,7 +509,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
             tmap, pd, ta, d_groups, d_ent, nstates, ntiles);
         CK(cudaGetLastError());
         CK(cudaEventRecord(e1, E.stream));
-        E.timed.push_back({e0, e1, true, bytes});
+        E.timed.push_back({e0, e1, true, bytes, pd.m0, pd.nm, nstates, ntiles});
         E.stats[0] += 1;
         E.stats[4] += bytes;
         E.stats[12] += 1;
@@ -507,7 +535,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     fn<<<(unsigned)blocks, threads, smem, E.stream>>>(pd, d_groups, d_ent, nstates, 0, e2);
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, E.stream));
-    E.timed.push_back({e0, e1, false, bytes});
+    E.timed.push_back({e0, e1, false, bytes, pd.m0, pd.nm, nstates, ntiles});
     E.stats[0] += 1;
     E.stats[4] += bytes;
     // algorithmic FP64/FP32 work: 2^(n-1) pairs x 28 flops per fused 2x2
@@ -1132,6 +1160,7 @@ void execute(Engine& E, const qv_circuits* c, const qv_results* r, double* out, 
     }
     E.stats[5] = ms;
     E.stats[14] = tma_ms;
+    log_launches(E);
 }
 
 // ---------------------------------------------------------------------------
@@ -1352,6 +1381,7 @@ void shift_js(Engine& E, const qv_circuits* c, int64_t nshift, const int64_t* ga
     }
     E.stats[5] = ms;
     E.stats[14] = tma_ms;
+    log_launches(E);
 }
 
 }  // namespace qvb

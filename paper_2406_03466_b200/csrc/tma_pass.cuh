@@ -58,6 +58,7 @@ struct TmaArgs {
     uint64_t state_bytes;
     uint32_t tile_bytes, mat_bytes;
     uint32_t tmat_off;        // direct stores: byte offset of the teams' matrix buffers
+    uint32_t ent_off;         // byte offset of the launch's (in, out, mats) table in shared memory
 };
 
 template <int STAGES>
@@ -175,10 +176,15 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     // the item's load, before the arrival that releases them with the tile
     __shared__ int32_t soc[STAGES][5];
     __shared__ V* sout[STAGES];
+    // the launch's state pointers, staged once: the thread that issues a load
+    // never waits on a global read in the middle of an item
+    const uint64_t* sent = reinterpret_cast<const uint64_t*>(smem_raw + ta.ent_off);
     auto issue_load = [&](int i) {
         const int w = (int)blockIdx.x + i * G;
         const int x = w / nstates, y = w - x * nstates;
-        const LaunchEntry e = ent[y];
+        struct { const void* in; void* out; const void* mats; } e = {
+            reinterpret_cast<const void*>(sent[3 * y]), reinterpret_cast<void*>(sent[3 * y + 1]),
+            reinterpret_cast<const void*>(sent[3 * y + 2])};
         uint64_t o = 0;   // outer offset of tile x (light-cone restricted passes list fewer bits)
         for (int j = 0; j < pd.n_outer; ++j)
             if ((x >> j) & 1) o |= 1ull << pd.obits[j];
@@ -200,6 +206,13 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
         uint4* gdst = reinterpret_cast<uint4*>(sg);
         for (int i = threadIdx.x; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
+        uint64_t* se = reinterpret_cast<uint64_t*>(smem_raw + ta.ent_off);
+        for (int y = threadIdx.x; y < nstates; y += blockDim.x) {
+            se[3 * y] = reinterpret_cast<uint64_t>(ent[y].in);
+            se[3 * y + 1] = reinterpret_cast<uint64_t>(ent[y].out);
+            se[3 * y + 2] = reinterpret_cast<uint64_t>(ent[y].mats);
+        }
+        __syncthreads();
         if (threadIdx.x == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(full0 + 8 * s, 1);
