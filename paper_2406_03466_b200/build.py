@@ -54,6 +54,15 @@ def build_product(force: bool = False, verbose_ptxas: bool = False) -> Path:
     return PRODUCT
 
 
+TRACE = PKG / "libqvb200_trace.so"
+
+
+def build_trace(force: bool = False) -> Path:
+    """Diagnostic build: tma_pass_kernel records a %clock64 timeline of its
+    first items (tools/tma_trace.py); select it with QVB200_LIB=<path>."""
+    return build_variant("trace", ["QV_TMA_TRACE"], force)
+
+
 def build_variant(name: str, defines: list[str], force: bool = False) -> Path:
     """Experimental build with extra -D tuning macros (QV_C128_TILE_BITS, ...),
     selected at run time with QVB200_LIB=<path>.  Used by A/B measurements."""

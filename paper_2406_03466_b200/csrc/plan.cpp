@@ -13,7 +13,9 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <functional>
 #include <stdexcept>
 #include <unordered_map>
@@ -259,6 +261,10 @@ struct GroupBuilder {
         return best;
     }
 
+    // false: keep segments maximal (fewer CTA barriers) and only choose their
+    // warp bits for the banks -- QVB200_PLAN_SEGMENTS=max, an A/B knob
+    bool split_on_bank_loss = !(getenv("QVB200_PLAN_SEGMENTS") && std::string(getenv("QVB200_PLAN_SEGMENTS")) == "max");
+
     void emit(std::vector<GroupDesc>& out) {
         const int tb = k - rbits;
         const int nwb = tb > 5 ? tb - 5 : 0;           // warp-index bits
@@ -320,7 +326,7 @@ struct GroupBuilder {
                 if (__builtin_popcount(f) < nwb) break;
                 const auto ext = best_w(s, e + 1, f);
                 const auto solo = best_w(e, e + 1, solo_free(e));
-                if (ext.first < cur.first + solo.first) break;
+                if (split_on_bank_loss && ext.first < cur.first + solo.first) break;
                 free_bits = f;
                 cur = ext;
                 ++e;

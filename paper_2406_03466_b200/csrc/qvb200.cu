@@ -473,6 +473,16 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         }
         gdim[0] *= elems0;
         box[0] *= elems0;
+        // QVB200_TMA_PIECES = 2 / 4 moves a tile as that many boxes along its
+        // outermost box dimension, so a stage's store read-out and the next
+        // load overlap piece by piece.  Measured on B200: 28q x 8L gradient
+        // 33.66 s (4 pieces) vs 33.69 s (1), 32q x 4L complex64 7.62 s vs
+        // 6.70 s -- whole-tile boxes by default.
+        static const int max_pieces = getenv("QVB200_TMA_PIECES") ? std::max(1, atoi(getenv("QVB200_TMA_PIECES"))) : 1;
+        int pieces = 1;
+        if (tl->ndim > 1)
+            while (pieces < max_pieces && pieces * 2 <= (int)box[tl->ndim - 1] && pieces * 2 <= 4) pieces *= 2;
+        box[tl->ndim - 1] /= pieces;
         ta.elems0 = elems0;
         gdim[tl->ndim] = (cuuint64_t)arena->slots;
         box[tl->ndim] = 1;
@@ -497,6 +507,8 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         }
         ta.tmat_off = (uint32_t)tmat_off;
         ta.ent_off = (uint32_t)ent_off;
+        ta.pieces = pieces;
+        ta.piece_step = (int32_t)box[tl->ndim - 1];
         ta.base = arena->base;
         ta.state_bytes = arena->state_bytes;
         ta.tile_bytes = (uint32_t)tile_bytes;
@@ -504,10 +516,39 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         const int64_t items = ntiles * nstates;
         if (items >= (1ll << 31)) throw ArgError("launch has too many (state, tile) items");
         const int64_t blocks = std::min<int64_t>(items, sms);
+        ta.trace = nullptr;
+#ifdef QV_TMA_TRACE
+        // trace the QVB200_TMA_TRACE_LAUNCH-th TMA launch of the process into
+        // $QVB200_TMA_TRACE (raw int64: a header, then the clock table)
+        static int tma_launch_no = 0;
+        static const int want = getenv("QVB200_TMA_TRACE_LAUNCH") ? atoi(getenv("QVB200_TMA_TRACE_LAUNCH")) : 5;
+        long long* d_trace = nullptr;
+        const size_t trace_n = (size_t)kTraceCtas * 2 * kTraceItems * 16;
+        const bool do_trace = getenv("QVB200_TMA_TRACE") && tma_launch_no++ == want;
+        if (do_trace) {
+            CK(cudaMalloc(&d_trace, trace_n * sizeof(long long)));
+            CK(cudaMemsetAsync(d_trace, 0, trace_n * sizeof(long long), E.stream));
+            ta.trace = d_trace;
+        }
+#endif
         CK(cudaEventRecord(e0, E.stream));
         tma_kernel<T>(teams, direct)<<<(unsigned)blocks, tma_threads(teams), tma_smem, E.stream>>>(
             tmap, pd, ta, d_groups, d_ent, nstates, ntiles);
         CK(cudaGetLastError());
+#ifdef QV_TMA_TRACE
+        if (do_trace) {
+            std::vector<long long> h(trace_n);
+            CK(cudaStreamSynchronize(E.stream));
+            CK(cudaMemcpy(h.data(), d_trace, trace_n * sizeof(long long), cudaMemcpyDeviceToHost));
+            cudaFree(d_trace);
+            if (FILE* f = fopen(getenv("QVB200_TMA_TRACE"), "wb")) {
+                const long long hdr[8] = {pd.nm, pd.ng, nstates, (long long)ntiles, blocks, teams, ta.pieces, kTraceItems};
+                fwrite(hdr, sizeof(long long), 8, f);
+                fwrite(h.data(), sizeof(long long), h.size(), f);
+                fclose(f);
+            }
+        }
+#endif
         CK(cudaEventRecord(e1, E.stream));
         E.timed.push_back({e0, e1, true, bytes, pd.m0, pd.nm, nstates, ntiles});
         E.stats[0] += 1;

@@ -59,7 +59,31 @@ struct TmaArgs {
     uint32_t tile_bytes, mat_bytes;
     uint32_t tmat_off;        // direct stores: byte offset of the teams' matrix buffers
     uint32_t ent_off;         // byte offset of the launch's (in, out, mats) table in shared memory
+    int32_t pieces;           // a tile moves as `pieces` boxes split along the outermost box dimension
+    int32_t piece_step;       // coordinate step between pieces along dimension ndim - 1
+    long long* trace;         // QV_TMA_TRACE builds only (tools/tma_trace.py), else null
 };
+
+// QV_TMA_TRACE (diagnostic build, libqvb200_trace.so): %clock64 of each phase
+// of the first kTraceItems items of each team of CTAs 0..kTraceCtas-1:
+// trace[((cta * 2 + team) * kTraceItems + item) * 16 + event], event 0 = wait
+// for the tile starts, 1 = tile resident, 2 + g = group g done, 12 = store
+// issued, 13 = next load issued, 14 = item done.
+constexpr int kTraceCtas = 4, kTraceItems = 64;
+#ifdef QV_TMA_TRACE
+#define TMA_MARK(item, ev)                                                                             \
+    do {                                                                                             \
+        if (ta.trace && blockIdx.x < kTraceCtas && (item) / TEAMS < kTraceItems && tid == 0) {     \
+            long long t_;                                                                            \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));                                       \
+            ta.trace[((blockIdx.x * 2 + team) * kTraceItems + (item) / TEAMS) * 16 + (ev)] = t_;    \
+        }                                                                                            \
+    } while (0)
+#else
+#define TMA_MARK(item, ev) \
+    do {                   \
+    } while (0)
+#endif
 
 template <int STAGES>
 struct TmaSmem {   // byte offsets inside dynamic shared memory
@@ -122,6 +146,15 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// wait until at most n (0..3) of this thread's bulk groups still read shared memory
+__device__ __forceinline__ void bulk_wait_read(int n) {
+    switch (n) {
+        case 0: asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); break;
+        case 1: asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); break;
+        case 2: asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group.read 3;\n" ::: "memory"); break;
+    }
+}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void team_sync(int team) {
@@ -176,6 +209,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     // the item's load, before the arrival that releases them with the tile
     __shared__ int32_t soc[STAGES][5];
     __shared__ V* sout[STAGES];
+    int32_t lc[5];        // load coordinates of the item being issued (issuing thread)
+    uint32_t lbar = 0;    // and its full barrier
     // the launch's state pointers, staged once: the thread that issues a load
     // never waits on a global read in the middle of an item
     const uint64_t* sent = reinterpret_cast<const uint64_t*>(smem_raw + ta.ent_off);
@@ -198,9 +233,37 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         c[ta.ndim] = (int32_t)(((const unsigned char*)e.in - ta.base) / ta.state_bytes);
         const uint32_t bar = full0 + 8 * full_of<STAGES>(i);
         mbar_expect_tx(bar, TILE + ta.mat_bytes);
-        tma_load_5d(sbase + s * TILE, &tmap, c, bar);
         bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes, reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4,
                   ta.mat_bytes, bar);
+        for (int d = 0; d < 5; ++d) lc[d] = c[d];
+        lbar = bar;
+    };
+    // The tile as `pieces` boxes (split along the outermost box dimension,
+    // contiguous in shared memory): a stage's store and the load that reuses
+    // it overlap piece by piece -- piece q of the next item loads as soon as
+    // piece q of the last one has been read out.
+    const uint32_t PIECE = TILE / (uint32_t)ta.pieces;
+    auto load_piece = [&](int s, int q) {
+        int32_t c[5] = {lc[0], lc[1], lc[2], lc[3], lc[4]};
+        c[ta.ndim - 1] += q * ta.piece_step;
+        tma_load_5d(sbase + s * TILE + q * PIECE, &tmap, c, lbar);
+    };
+    auto store_piece = [&](int s, int q) {
+        int32_t c[5] = {soc[s][0], soc[s][1], soc[s][2], soc[s][3], soc[s][4]};
+        c[ta.ndim - 1] += q * ta.piece_step;
+        tma_store_5d(&tmap, c, sbase + s * TILE + q * PIECE);
+        bulk_commit();
+    };
+    // store the item in stage s, then load item `next` (if any) into it
+    auto turn_stage = [&](int s, int next) {
+        for (int q = 0; q < ta.pieces; ++q) store_piece(s, q);
+        if (next < my_items) {
+            issue_load(next);
+            for (int q = 0; q < ta.pieces; ++q) {
+                bulk_wait_read(ta.pieces - 1 - q);   // piece q of the store has left shared memory
+                load_piece(s, q);
+            }
+        }
     };
     {
         const uint4* gsrc = reinterpret_cast<const uint4*>(gdesc + pd.g0);
@@ -222,7 +285,10 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             fence_proxy_async_smem();
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
-            for (int i = 0; i < STAGES && i < my_items; ++i) issue_load(i);
+            for (int i = 0; i < STAGES && i < my_items; ++i) {
+                issue_load(i);
+                for (int q = 0; q < ta.pieces; ++q) load_piece(i % STAGES, q);
+            }
         }
     }
     __syncthreads();
@@ -233,12 +299,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         for (int j = 0; j < my_items; ++j) {
             const int s = j % STAGES;
             mbar_wait(done0 + 8 * s, (uint32_t)((j / STAGES) & 1));
-            tma_store_5d(&tmap, soc[s], sbase + s * TILE);
-            bulk_commit();
-            if (j + STAGES < my_items) {
-                bulk_wait_read0();   // the stage's bytes have left shared memory
-                issue_load(j + STAGES);
-            }
+            turn_stage(s, j + STAGES);
         }
         bulk_wait0();   // every store has completed before the CTA retires
         return;
@@ -257,7 +318,9 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         }
     for (int i = team; i < my_items; i += TEAMS) {
         const int s = i % STAGES;
+        TMA_MARK(i, 0);
         mbar_wait(full0 + 8 * full_of<STAGES>(i), full_parity<STAGES>(i));
+        TMA_MARK(i, 1);
         const uint32_t boff = s * TILE;   // a multiple of 2^15 >= every slot offset
         const V* smat = reinterpret_cast<const V*>(smem_raw + STAGES * TILE + s * kTmaMatBytes);
         V* __restrict__ out = nullptr;
@@ -298,7 +361,10 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 // every thread of the team has read the stage: hand it to the
                 // load of item i + STAGES
                 team_sync(team);
-                if (tid == 0 && i + STAGES < my_items) issue_load(i + STAGES);
+                if (tid == 0 && i + STAGES < my_items) {
+                    issue_load(i + STAGES);
+                    for (int q = 0; q < ta.pieces; ++q) load_piece(s, q);
+                }
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -313,6 +379,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                         if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
                 }
             }
+            if (g < 10) TMA_MARK(i, 2 + g);
             if (!last) {
 #pragma unroll
                 for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off(j)) = a[j];
@@ -336,14 +403,9 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 mbar_arrive(done0 + 8 * s);
             } else {
                 team_sync(team);
-                if (tid == 0) {
-                    tma_store_5d(&tmap, soc[s], sbase + s * TILE);
-                    bulk_commit();
-                    if (i + STAGES < my_items) {
-                        bulk_wait_read0();   // this thread's store has read the stage
-                        issue_load(i + STAGES);
-                    }
-                }
+                TMA_MARK(i, 12);
+                if (tid == 0) turn_stage(s, i + STAGES);
+                TMA_MARK(i, 13);
             }
         }
     }
