@@ -366,10 +366,22 @@ bool tma_direct() {
     static const bool d = getenv("QVB200_TMA_DIRECT") && std::string(getenv("QVB200_TMA_DIRECT")) == "1";
     return d;
 }
+// Two teams: the thread of the team that stored a stage reloads it (complex128
+// default), or a producer warpgroup does (complex64 default); QVB200_TMA_PWG =
+// 0 / 1 forces either.  Measured on B200: 28q x 8L complex128 gradient 33.3-
+// 33.6 s (team thread) vs 34.4-35.2 s (producer warpgroup: both teams then
+// run their groups in phase); 32q x 4L complex64 6.55-6.72 s vs 6.39 s.
+bool tma_pwg(int precision) {
+    static const char* env = getenv("QVB200_TMA_PWG");
+    if (env) return std::string(env) == "1";
+    return precision == 1;
+}
 template <typename T>
-TmaFn tma_kernel(int teams, bool direct) {
-    if (teams == 1) return &tma_pass_kernel<T, tma_stages<T>(), 1, false>;
-    return direct ? &tma_pass_kernel<T, tma_stages<T>(), 2, true> : &tma_pass_kernel<T, tma_stages<T>(), 2, false>;
+TmaFn tma_kernel(int teams, bool direct, bool pwg) {
+    constexpr int ST = tma_stages<T>();
+    if (teams == 1) return &tma_pass_kernel<T, ST, 1, false, false>;
+    if (direct) return &tma_pass_kernel<T, ST, 2, true, false>;
+    return pwg ? &tma_pass_kernel<T, ST, 2, false, true> : &tma_pass_kernel<T, ST, 2, false, false>;
 }
 constexpr size_t kTmaSmemCap = 226 * 1024;   // 227 KiB per block less the kernel's static stage table
 
@@ -381,8 +393,9 @@ void set_kernel_attributes() {
         CK(cudaFuncSetAttribute(pass_kernel_multi<T>(pair), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (int teams : {1, 2})
         for (bool direct : {false, true})
-            CK(cudaFuncSetAttribute(tma_kernel<T>(teams, direct), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kTmaSmemCap));
+            for (bool pwg : {false, true})
+                CK(cudaFuncSetAttribute(tma_kernel<T>(teams, direct, pwg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kTmaSmemCap));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -452,6 +465,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     constexpr int ST = tma_stages<T>();
     const int teams = tma_teams();
     const bool direct = teams > 1 && tma_direct();
+    const bool pwg = teams > 1 && !direct && tma_pwg(E.precision);
     const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
     const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);
     const size_t tma_smem = ent_off + (size_t)nstates * 3 * sizeof(uint64_t);
@@ -532,7 +546,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         }
 #endif
         CK(cudaEventRecord(e0, E.stream));
-        tma_kernel<T>(teams, direct)<<<(unsigned)blocks, tma_threads(teams), tma_smem, E.stream>>>(
+        tma_kernel<T>(teams, direct, pwg)<<<(unsigned)blocks, tma_threads(teams, pwg), tma_smem, E.stream>>>(
             tmap, pd, ta, d_groups, d_ent, nstates, ntiles);
         CK(cudaGetLastError());
 #ifdef QV_TMA_TRACE

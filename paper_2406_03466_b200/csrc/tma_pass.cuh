@@ -41,7 +41,15 @@ constexpr int kTmaTeamThreads = 256;       // 2^(12 - 4): one register group cov
 // 17th warp would cut every warp's register share, allocated in 4-warp
 // units, to 96); the team that finishes an item issues its store and the
 // load that reuses the stage (see tma_pass_kernel).
-__host__ __device__ constexpr int tma_threads(int teams) { return teams == 1 ? kTmaTeamThreads + 32 : 2 * kTmaTeamThreads; }
+// With PWG (two teams + a producer warpgroup: 640 threads) the launch gets
+// 96 registers per thread; the producer warpgroup gives most of its share back
+// (setmaxnreg 24) and the compute warpgroups take 112 -- within the CTA's
+// pool of 96 x 640 (asking for more than the pool holds never returns).
+__host__ __device__ constexpr int tma_threads(int teams, bool pwg = false) {
+    return teams == 1 ? kTmaTeamThreads + 32 : 2 * kTmaTeamThreads + (pwg ? 128 : 0);
+}
+constexpr int kPwgComputeRegs = 112, kPwgProducerRegs = 24;
+static_assert(2 * kTmaTeamThreads * kPwgComputeRegs + 128 * kPwgProducerRegs <= 96 * 640, "setmaxnreg pool");
 constexpr int kTmaMatBytes = 4096;         // per-stage matrix area (<= 64 complex128 matrices)
 
 // Per-launch constants of the TMA kernel (passed by value).
@@ -182,11 +190,13 @@ __device__ __forceinline__ void team_sync(int team) {
 //    one bulk-tensor store sends it; once the store has read the stage, the
 //    load of item i + STAGES is issued (by the producer warp for TEAMS = 1,
 //    signalled by done[], or by an elected thread of the team for TEAMS = 2).
-template <typename T, int STAGES, int TEAMS, bool DIRECT>
-__global__ void __launch_bounds__(tma_threads(TEAMS), 1)
+template <typename T, int STAGES, int TEAMS, bool DIRECT, bool PWG>
+__global__ void __launch_bounds__(tma_threads(TEAMS, PWG), 1)
 tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, const TmaArgs ta,
                 const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent, int nstates, int64_t ntiles) {
     static_assert(!DIRECT || TEAMS > 1, "direct stores are issued by the teams themselves");
+    static_assert(!PWG || (TEAMS == 2 && !DIRECT), "the producer warpgroup serves two teams with bulk stores");
+    constexpr bool PRODUCER_THREAD = TEAMS == 1 || PWG;   // a thread outside the teams stores and reloads stages
     typedef typename Cx<T>::V V;
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
     constexpr int NA = 1 << R;
@@ -294,7 +304,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     __syncthreads();
 
     if (threadIdx.x >= COMPUTE) {
-        // --------------------------------------------- producer (TEAMS == 1)
+        // ------------------------------- producer (TEAMS == 1 or PWG)
+        if constexpr (PWG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kPwgProducerRegs) : "memory");
         if (threadIdx.x != COMPUTE) return;
         for (int j = 0; j < my_items; ++j) {
             const int s = j % STAGES;
@@ -306,6 +317,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     }
 
     // ---------------------------------------------------------------- compute
+    if constexpr (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPwgComputeRegs) : "memory");
     const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / kTmaTeamThreads);
     const int tid = (int)(threadIdx.x % kTmaTeamThreads);
     uint32_t wbase = 0;
@@ -381,8 +393,15 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             }
             if (g < 10) TMA_MARK(i, 2 + g);
             if (!last) {
+                // re-read the four register-bit columns (volatile: the 16 slot
+                // offsets are recomputed here instead of being held -- or
+                // spilled -- across the group's math)
+                const volatile uint32_t* vc = GD.combo;
+                const uint32_t sc0 = vc[1], sc1 = vc[2], sc2 = vc[4], sc3 = vc[8];
 #pragma unroll
-                for (int j = 0; j < NA; ++j) *reinterpret_cast<V*>(smem_raw + off(j)) = a[j];
+                for (int j = 0; j < NA; ++j)
+                    *reinterpret_cast<V*>(smem_raw + (base ^ ((j & 1) ? sc0 : 0u) ^ ((j & 2) ? sc1 : 0u) ^
+                                                      ((j & 4) ? sc2 : 0u) ^ ((j & 8) ? sc3 : 0u))) = a[j];
                 if (!sg[g + 1].cta_sync) __syncwarp();
                 else team_sync(team);
             } else if constexpr (DIRECT) {
@@ -399,7 +418,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         }
         if constexpr (!DIRECT) {
             fence_proxy_async_smem();   // generic-proxy writes -> visible to the TMA store
-            if constexpr (TEAMS == 1) {
+            if constexpr (PRODUCER_THREAD) {
                 mbar_arrive(done0 + 8 * s);
             } else {
                 team_sync(team);
@@ -409,7 +428,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             }
         }
     }
-    if constexpr (TEAMS > 1 && !DIRECT) {
+    if constexpr (!PRODUCER_THREAD && !DIRECT) {
         if (tid == 0) bulk_wait0();   // this team's stores have completed
     }
 }

@@ -33,8 +33,9 @@ def main():
                 for g in range(int(ng)):
                     r[f"g{g}"] = e[2 + g] - prev
                     prev = e[2 + g]
-                r["tail"] = e[12] - prev          # last group's stores + fence + barrier
-                r["turn"] = e[13] - e[12]         # store issue, read-out wait, next load issue
+                if e[12]:   # the team's own thread stores and reloads the stage
+                    r["tail"] = e[12] - prev      # last group's stores + fence + barrier
+                    r["turn"] = e[13] - e[12]     # store issue, read-out wait, next load issue
                 r["period"] = nxt[0] - e[0]
                 rows.append(r)
         if not rows:
