@@ -376,12 +376,19 @@ bool tma_pwg(int precision) {
     if (env) return std::string(env) == "1";
     return precision == 1;
 }
+// QVB200_TMA_ALT=1: the two teams take turns on the FP64 pipe (producer
+// warpgroup or direct-store kernels only).
+bool tma_alt() {
+    static const bool a = getenv("QVB200_TMA_ALT") && std::string(getenv("QVB200_TMA_ALT")) == "1";
+    return a;
+}
 template <typename T>
-TmaFn tma_kernel(int teams, bool direct, bool pwg) {
+TmaFn tma_kernel(int teams, bool direct, bool pwg, bool alt) {
     constexpr int ST = tma_stages<T>();
-    if (teams == 1) return &tma_pass_kernel<T, ST, 1, false, false>;
-    if (direct) return &tma_pass_kernel<T, ST, 2, true, false>;
-    return pwg ? &tma_pass_kernel<T, ST, 2, false, true> : &tma_pass_kernel<T, ST, 2, false, false>;
+    if (teams == 1) return &tma_pass_kernel<T, ST, 1, false, false, false>;
+    if (direct) return alt ? &tma_pass_kernel<T, ST, 2, true, false, true> : &tma_pass_kernel<T, ST, 2, true, false, false>;
+    if (pwg) return alt ? &tma_pass_kernel<T, ST, 2, false, true, true> : &tma_pass_kernel<T, ST, 2, false, true, false>;
+    return &tma_pass_kernel<T, ST, 2, false, false, false>;
 }
 constexpr size_t kTmaSmemCap = 226 * 1024;   // 227 KiB per block less the kernel's static stage table
 
@@ -394,8 +401,9 @@ void set_kernel_attributes() {
     for (int teams : {1, 2})
         for (bool direct : {false, true})
             for (bool pwg : {false, true})
-                CK(cudaFuncSetAttribute(tma_kernel<T>(teams, direct, pwg), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kTmaSmemCap));
+                for (bool alt : {false, true})
+                    CK(cudaFuncSetAttribute(tma_kernel<T>(teams, direct, pwg, alt),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemCap));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -466,6 +474,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const int teams = tma_teams();
     const bool direct = teams > 1 && tma_direct();
     const bool pwg = teams > 1 && !direct && tma_pwg(E.precision);
+    const bool alt = (direct || pwg) && tma_alt();
     const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
     const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);
     const size_t tma_smem = ent_off + (size_t)nstates * 3 * sizeof(uint64_t);
@@ -546,7 +555,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         }
 #endif
         CK(cudaEventRecord(e0, E.stream));
-        tma_kernel<T>(teams, direct, pwg)<<<(unsigned)blocks, tma_threads(teams, pwg), tma_smem, E.stream>>>(
+        tma_kernel<T>(teams, direct, pwg, alt)<<<(unsigned)blocks, tma_threads(teams, pwg), tma_smem, E.stream>>>(
             tmap, pd, ta, d_groups, d_ent, nstates, ntiles);
         CK(cudaGetLastError());
 #ifdef QV_TMA_TRACE

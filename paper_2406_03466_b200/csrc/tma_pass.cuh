@@ -97,7 +97,8 @@ template <int STAGES>
 struct TmaSmem {   // byte offsets inside dynamic shared memory
     __host__ __device__ static constexpr uint32_t full(uint32_t tile) { return STAGES * (tile + kTmaMatBytes); }
     __host__ __device__ static constexpr uint32_t done(uint32_t tile) { return full(tile) + 16 * STAGES; }
-    __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return (done(tile) + 8 * STAGES + 127) & ~127u; }
+    __host__ __device__ static constexpr uint32_t tok(uint32_t tile) { return done(tile) + 8 * STAGES; }
+    __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return (tok(tile) + 16 + 127) & ~127u; }
     __host__ __device__ static constexpr uint32_t bytes(uint32_t tile, int ng) { return groups(tile) + 128u * ng; }
 };
 // Item i's tile lands on full barrier full_of(i) = (stage, (i / STAGES) mod 2)
@@ -190,12 +191,21 @@ __device__ __forceinline__ void team_sync(int team) {
 //    one bulk-tensor store sends it; once the store has read the stage, the
 //    load of item i + STAGES is issued (by the producer warp for TEAMS = 1,
 //    signalled by done[], or by an elected thread of the team for TEAMS = 2).
-template <typename T, int STAGES, int TEAMS, bool DIRECT, bool PWG>
+//
+// ALT (two teams that never block on the TMA: producer warpgroup or direct
+// stores): the teams take turns on the FP64 pipe -- math phase k of team 1
+// waits for team 0's phase k, team 0's phase k + 1 for team 1's phase k
+// (two mbarriers, one arrival per thread after its math) -- so each team's
+// shared-memory loads, stores and barriers run under the other team's math
+// instead of in phase with it (both teams computing at once doubled every
+// group's time, QV_TMA_TRACE).
+template <typename T, int STAGES, int TEAMS, bool DIRECT, bool PWG, bool ALT>
 __global__ void __launch_bounds__(tma_threads(TEAMS, PWG), 1)
 tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, const TmaArgs ta,
                 const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent, int nstates, int64_t ntiles) {
     static_assert(!DIRECT || TEAMS > 1, "direct stores are issued by the teams themselves");
     static_assert(!PWG || (TEAMS == 2 && !DIRECT), "the producer warpgroup serves two teams with bulk stores");
+    static_assert(!ALT || PWG || DIRECT, "alternating math needs teams that never wait on the TMA");
     constexpr bool PRODUCER_THREAD = TEAMS == 1 || PWG;   // a thread outside the teams stores and reloads stages
     typedef typename Cx<T>::V V;
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
@@ -209,6 +219,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     GroupDesc* sg = reinterpret_cast<GroupDesc*>(smem_raw + TmaSmem<STAGES>::groups(TILE));
     const uint32_t full0 = sbase + TmaSmem<STAGES>::full(TILE);
     const uint32_t done0 = sbase + TmaSmem<STAGES>::done(TILE);
+    const uint32_t tok0 = sbase + TmaSmem<STAGES>::tok(TILE);
 
     const int items = (int)(ntiles * nstates);
     const int G = gridDim.x;
@@ -292,6 +303,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 mbar_init(full0 + 8 * (STAGES + s), 1);
                 mbar_init(done0 + 8 * s, kTmaTeamThreads);
             }
+            mbar_init(tok0, kTmaTeamThreads);
+            mbar_init(tok0 + 8, kTmaTeamThreads);
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             fence_proxy_async_smem();
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
@@ -320,6 +333,9 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     if constexpr (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPwgComputeRegs) : "memory");
     const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / kTmaTeamThreads);
     const int tid = (int)(threadIdx.x % kTmaTeamThreads);
+    // ALT: math phases of this team so far, and how many each team has in total
+    int phase = 0;
+    const int phases0 = ((my_items + 1) / 2) * pd.ng, phases1 = (my_items / 2) * pd.ng;
     uint32_t wbase = 0;
     uint64_t gbase = 0;
 #pragma unroll
@@ -379,7 +395,14 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 }
             }
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
+#ifndef QV_TMA_DIAG_NOMATH
+#define QV_TMA_DIAG_NOMATH 0   // diagnostic builds only: skip the 2x2 math (wrong results)
+#endif
+            if constexpr (ALT) {   // this team's turn on the FP64 pipe
+                if (team == 0 && phase >= 1 && phase <= phases1) mbar_wait(tok0, (uint32_t)((phase - 1) & 1));
+                if (team == 1 && phase < phases0) mbar_wait(tok0 + 8, (uint32_t)(phase & 1));
+            }
+            for (int r = 0; r < (QV_TMA_DIAG_NOMATH ? 0 : R); ++r) {
                 const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
                 if (mi >= 0) {
                     if (r > 0) {
@@ -390,6 +413,11 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                     for (int j = 0; j < NA; ++j)
                         if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
                 }
+            }
+            if constexpr (ALT) {   // hand the FP64 pipe to the other team
+                if (team == 0 && phase < phases0) mbar_arrive(tok0 + 8);
+                if (team == 1) mbar_arrive(tok0);
+                ++phase;
             }
             if (g < 10) TMA_MARK(i, 2 + g);
             if (!last) {
@@ -405,8 +433,10 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 if (!sg[g + 1].cta_sync) __syncwarp();
                 else team_sync(team);
             } else if constexpr (DIRECT) {
+                TMA_MARK(i, 12);
 #pragma unroll
                 for (int j = 0; j < NA; ++j) __stcs(out + (gbase ^ ta.gwcombo[j]), a[j]);
+                TMA_MARK(i, 13);
             } else {
                 // every thread of the team has read its amplitudes before any
                 // is rewritten in the TMA box layout
