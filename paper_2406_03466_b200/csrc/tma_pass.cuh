@@ -78,6 +78,9 @@ struct TmaArgs {
 // for the tile starts, 1 = tile resident, 2 + g = group g done, 12 = store
 // issued, 13 = next load issued, 14 = item done.
 constexpr int kTraceCtas = 4, kTraceItems = 64;
+#ifndef QV_TMA_DIAG_NOMATH
+#define QV_TMA_DIAG_NOMATH 0   // diagnostic builds only: skip the 2x2 math (wrong results)
+#endif
 #ifdef QV_TMA_TRACE
 #define TMA_MARK(item, ev)                                                                             \
     do {                                                                                             \
@@ -301,10 +304,10 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(full0 + 8 * s, 1);
                 mbar_init(full0 + 8 * (STAGES + s), 1);
-                mbar_init(done0 + 8 * s, kTmaTeamThreads);
+                mbar_init(done0 + 8 * s, kTmaTeamThreads / 32);   // one arrival per warp
             }
-            mbar_init(tok0, kTmaTeamThreads);
-            mbar_init(tok0 + 8, kTmaTeamThreads);
+            mbar_init(tok0, kTmaTeamThreads / 32);
+            mbar_init(tok0 + 8, kTmaTeamThreads / 32);
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             fence_proxy_async_smem();
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
@@ -382,8 +385,16 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 return base ^ ((j & 1) ? rc0 : 0u) ^ ((j & 2) ? rc1 : 0u) ^ ((j & 4) ? rc2 : 0u) ^ ((j & 8) ? rc3 : 0u);
             };
             V a[NA];
+#ifndef QV_TMA_DIAG_NOSMEM
+#define QV_TMA_DIAG_NOSMEM 0   // diagnostic builds only: registers instead of the group's smem round trip
+#endif
+            if (QV_TMA_DIAG_NOSMEM && g > 0) {
 #pragma unroll
-            for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off(j));
+                for (int j = 0; j < NA; ++j) a[j] = V{T(j + tid), T(g)};
+            } else {
+#pragma unroll
+                for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off(j));
+            }
             const bool last = g + 1 == pd.ng;
             if (DIRECT && last) {
                 // every thread of the team has read the stage: hand it to the
@@ -394,14 +405,11 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                     for (int q = 0; q < ta.pieces; ++q) load_piece(s, q);
                 }
             }
-#pragma unroll
-#ifndef QV_TMA_DIAG_NOMATH
-#define QV_TMA_DIAG_NOMATH 0   // diagnostic builds only: skip the 2x2 math (wrong results)
-#endif
             if constexpr (ALT) {   // this team's turn on the FP64 pipe
                 if (team == 0 && phase >= 1 && phase <= phases1) mbar_wait(tok0, (uint32_t)((phase - 1) & 1));
                 if (team == 1 && phase < phases0) mbar_wait(tok0 + 8, (uint32_t)(phase & 1));
             }
+#pragma unroll
             for (int r = 0; r < (QV_TMA_DIAG_NOMATH ? 0 : R); ++r) {
                 const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
                 if (mi >= 0) {
@@ -415,12 +423,21 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 }
             }
             if constexpr (ALT) {   // hand the FP64 pipe to the other team
-                if (team == 0 && phase < phases0) mbar_arrive(tok0 + 8);
-                if (team == 1) mbar_arrive(tok0);
+                // one arrival per warp (256 arrivals on one word serialise)
+                __syncwarp();
+                if ((tid & 31) == 0) {
+                    if (team == 0 && phase < phases0) mbar_arrive(tok0 + 8);
+                    if (team == 1) mbar_arrive(tok0);
+                }
                 ++phase;
             }
             if (g < 10) TMA_MARK(i, 2 + g);
-            if (!last) {
+            if (!last && QV_TMA_DIAG_NOSMEM) {
+                // diagnostic: keep the results live without the smem store
+                if (a[0].x == T(-12345.678)) *reinterpret_cast<V*>(smem_raw + off(0)) = a[1];
+                if (!sg[g + 1].cta_sync) __syncwarp();
+                else team_sync(team);
+            } else if (!last) {
                 // re-read the four register-bit columns (volatile: the 16 slot
                 // offsets are recomputed here instead of being held -- or
                 // spilled -- across the group's math)
@@ -449,7 +466,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         if constexpr (!DIRECT) {
             fence_proxy_async_smem();   // generic-proxy writes -> visible to the TMA store
             if constexpr (PRODUCER_THREAD) {
-                mbar_arrive(done0 + 8 * s);
+                __syncwarp();   // the warp's fenced writes, then one arrival per warp
+                if ((tid & 31) == 0) mbar_arrive(done0 + 8 * s);
             } else {
                 team_sync(team);
                 TMA_MARK(i, 12);

@@ -260,3 +260,51 @@ def test_mcvqe_row_fast_path_matches_reference(golden_small, n_vqpus):
     rep = qv.mcvqe_gradient(ham, spec, qv.VqpuPoolConfig(n_virtual_qpus=n_vqpus), backend_factory=lambda: backend)
     assert rep.n_circuit_executions == case["n_circuits"]
     assert np.max(np.abs(np.asarray(rep.gradient) - case["gradient"])) < 1e-10
+
+
+def test_foreign_circuits_lowered_like_a_per_gate_loop():
+    """Reference-shaped circuits (duck-typed .gates with .kind.value /
+    .targets / .angle, e.g. qvirt.Circuit) lower through the topology-reusing
+    fast path to exactly the arrays a per-gate loop gives; a changed topology
+    in the middle of a batch is detected; unbound parameters are rejected."""
+    import enum
+    from types import SimpleNamespace as NS
+
+    from paper_2406_03466_b200.backend import lower_batch
+    from paper_2406_03466_b200.ir import CODE_BY_VALUE
+
+    class Kind(enum.Enum):
+        H = "h"
+        CNOT = "cnot"
+        RY = "ry"
+        RZ = "rz"
+
+    def circ(angles, extra=False):
+        gates = [NS(kind=Kind.H, targets=(0,), angle=None), NS(kind=Kind.CNOT, targets=(0, 1), angle=None)]
+        gates += [NS(kind=Kind.RZ if i % 2 else Kind.RY, targets=(i % 3,), angle=a) for i, a in enumerate(angles)]
+        if extra:
+            gates.append(NS(kind=Kind.CNOT, targets=(2, 1), angle=None))
+        return NS(gates=tuple(gates), n_qubits=3, name="f")
+
+    batch = [circ([0.1 * k + j for j in range(5)]) for k in range(4)] + [circ([1.0, 2.0, 3.0, 4.0, 5.0], extra=True)]
+    lb = lower_batch(batch)
+    for ci, c in enumerate(batch):
+        o0, o1 = lb.gate_offsets[ci], lb.gate_offsets[ci + 1]
+        want_k = [CODE_BY_VALUE[g.kind.value] for g in c.gates]
+        want_a = [g.angle if g.angle is not None else 0.0 for g in c.gates]
+        want_q0 = [g.targets[0] for g in c.gates]
+        want_q1 = [g.targets[1] if len(g.targets) > 1 else -1 for g in c.gates]
+        assert lb.kinds[o0:o1].tolist() == want_k
+        assert lb.angles[o0:o1].tolist() == want_a
+        assert lb.q0[o0:o1].tolist() == want_q0
+        assert lb.q1[o0:o1].tolist() == want_q1
+    with pytest.raises(ValueError, match="unbound"):
+        lower_batch([circ([0.1, "t1", 0.3, 0.4, 0.5])])
+
+
+def test_support_keys_of_mixed_width_rejected():
+    """'0' + '111' joins to n * len bits for n = 2 but is not a 2-qubit support."""
+    from paper_2406_03466_b200.backend import support_indices
+    with pytest.raises(ValueError):
+        support_indices(["0", "111"], 2)
+    assert support_indices(["01", "11", "00"], 2).tolist() == [0, 1, 3]
