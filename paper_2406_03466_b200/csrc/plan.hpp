@@ -32,16 +32,16 @@ constexpr int kGroupAmps = 1 << kRegBits;
 __host__ __device__
 #endif
 constexpr int reg_bits(int precision) { return precision == 0 ? QV_C128_REG_BITS : 4; }
-// Widest tile (multi-tile registers): 2^12 amplitudes for both precisions
-// (64 KiB complex128, 32 KiB complex64).  Measured on B200: complex128 at 13
-// bits (128 KiB, one CTA per SM) and 11 bits (more passes) are slower; for
-// complex64, 12 bits with three CTAs per SM beat 13 bits with one (32q x 4L
-// gradient 9.6 s vs 10.1 s).
+// Widest tile (multi-tile registers): 64 KiB for both precisions -- 2^12
+// complex128 / 2^13 complex64 amplitudes, three of them in the TMA kernel's
+// shared-memory ring.  (complex128 at 13 bits, 128 KiB, leaves room for no
+// ring; 11 bits needs 28 passes instead of 23 for 28q x 8L.  complex64 at 13
+// bits: 13 passes instead of 17 for 32q x 4L.)
 #ifndef QV_C128_TILE_BITS
 #define QV_C128_TILE_BITS 12
 #endif
 #ifndef QV_C64_TILE_BITS
-#define QV_C64_TILE_BITS 12
+#define QV_C64_TILE_BITS 13
 #endif
 #ifdef __CUDACC__
 __host__ __device__

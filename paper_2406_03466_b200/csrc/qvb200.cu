@@ -348,7 +348,9 @@ PassFn<T> pass_kernel_multi(bool pair) {
 // TMA pass kernel: stages in flight per CTA (one CTA per SM).  complex128
 // tiles are 64 KiB (3 stages), complex64 tiles 32 KiB (5 stages).
 template <typename T>
-constexpr int tma_stages() { return sizeof(T) == 8 ? 3 : 5; }
+constexpr int tma_stages() {   // 64 KiB tiles: 3 stages, 32 KiB: 5
+    return (sizeof(typename Cx<T>::V) << max_tile_bits(sizeof(T) == 8 ? 0 : 1)) >= 65536 ? 3 : 5;
+}
 typedef void (*TmaFn)(const CUtensorMap, const PassDesc, const TmaArgs, const GroupDesc*, const LaunchEntry*, int,
                       int64_t);
 // Compute teams per CTA (QVB200_TMA_TEAMS = 1 or 2, default 2).
@@ -385,10 +387,17 @@ bool tma_alt() {
 template <typename T>
 TmaFn tma_kernel(int teams, bool direct, bool pwg, bool alt) {
     constexpr int ST = tma_stages<T>();
-    if (teams == 1) return &tma_pass_kernel<T, ST, 1, false, false, false>;
-    if (direct) return alt ? &tma_pass_kernel<T, ST, 2, true, false, true> : &tma_pass_kernel<T, ST, 2, true, false, false>;
-    if (pwg) return alt ? &tma_pass_kernel<T, ST, 2, false, true, true> : &tma_pass_kernel<T, ST, 2, false, true, false>;
-    return &tma_pass_kernel<T, ST, 2, false, false, false>;
+    constexpr int TBI = multi_tile_tb<T>();
+    if constexpr (TBI != 8) {   // 512-thread tiles: one team + the producer warp
+        return &tma_pass_kernel<T, TBI, ST, 1, false, false, false>;
+    } else {
+        if (teams == 1) return &tma_pass_kernel<T, 8, ST, 1, false, false, false>;
+        if (direct)
+            return alt ? &tma_pass_kernel<T, 8, ST, 2, true, false, true> : &tma_pass_kernel<T, 8, ST, 2, true, false, false>;
+        if (pwg)
+            return alt ? &tma_pass_kernel<T, 8, ST, 2, false, true, true> : &tma_pass_kernel<T, 8, ST, 2, false, true, false>;
+        return &tma_pass_kernel<T, 8, ST, 2, false, false, false>;
+    }
 }
 constexpr size_t kTmaSmemCap = 226 * 1024;   // 227 KiB per block less the kernel's static stage table
 
@@ -471,14 +480,14 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const size_t tile_bytes = sizeof(V) << pd.k;
     const size_t mat_bytes = (size_t)pd.nm * 4 * sizeof(V);
     constexpr int ST = tma_stages<T>();
-    const int teams = tma_teams();
+    const int teams = multi_tile_tb<T>() == 8 ? tma_teams() : 1;
     const bool direct = teams > 1 && tma_direct();
     const bool pwg = teams > 1 && !direct && tma_pwg(E.precision);
     const bool alt = (direct || pwg) && tma_alt();
     const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
     const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);
     const size_t tma_smem = ent_off + (size_t)nstates * 3 * sizeof(uint64_t);
-    if (tl && tl->ok && arena && arena->base && multi && tb == 8 && ep.flags == F_STORE && pd.fresh == 0 &&
+    if (tl && tl->ok && arena && arena->base && multi && tb == multi_tile_tb<T>() && ep.flags == F_STORE && pd.fresh == 0 &&
         !generated && pd.ng >= 1 && mat_bytes <= (size_t)kTmaMatBytes && tma_smem <= kTmaSmemCap && tma_enabled() &&
         encode_tiled()) {
         TmaArgs ta;
@@ -524,7 +533,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
             ta.wcombo[j] = tl->wcombo[j];
             ta.gwcombo[j] = tl->gwcombo[j];
         }
-        for (int m = 0; m < 8; ++m) {
+        for (int m = 0; m < 9; ++m) {
             ta.wtcol[m] = tl->wtcol[m];
             ta.gwtcol[m] = tl->gwtcol[m];
         }
@@ -555,7 +564,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
         }
 #endif
         CK(cudaEventRecord(e0, E.stream));
-        tma_kernel<T>(teams, direct, pwg, alt)<<<(unsigned)blocks, tma_threads(teams, pwg), tma_smem, E.stream>>>(
+        tma_kernel<T>(teams, direct, pwg, alt)<<<(unsigned)blocks, tma_threads(teams, pwg, multi_tile_tb<T>()), tma_smem, E.stream>>>(
             tmap, pd, ta, d_groups, d_ent, nstates, ntiles);
         CK(cudaGetLastError());
 #ifdef QV_TMA_TRACE

@@ -35,7 +35,8 @@
 
 namespace qvb {
 
-constexpr int kTmaTeamThreads = 256;       // 2^(12 - 4): one register group covers the tile
+constexpr int kTmaTeamThreads = 256;       // 2^(12 - 4): one register group covers a 12-bit tile
+// (complex64 tiles are 13 bits: one team of 2^(13 - 4) = 512 threads)
 // One team: 8 compute warps + a producer warp (288 threads).  Two teams: 16
 // compute warps and no producer warp (512 threads, 128 registers each -- a
 // 17th warp would cut every warp's register share, allocated in 4-warp
@@ -45,8 +46,8 @@ constexpr int kTmaTeamThreads = 256;       // 2^(12 - 4): one register group cov
 // 96 registers per thread; the producer warpgroup gives most of its share back
 // (setmaxnreg 24) and the compute warpgroups take 112 -- within the CTA's
 // pool of 96 x 640 (asking for more than the pool holds never returns).
-__host__ __device__ constexpr int tma_threads(int teams, bool pwg = false) {
-    return teams == 1 ? kTmaTeamThreads + 32 : 2 * kTmaTeamThreads + (pwg ? 128 : 0);
+__host__ __device__ constexpr int tma_threads(int teams, bool pwg = false, int tbits = 8) {
+    return teams == 1 ? (1 << tbits) + 32 : 2 * (1 << tbits) + (pwg ? 128 : 0);
 }
 constexpr int kPwgComputeRegs = 112, kPwgProducerRegs = 24;
 static_assert(2 * kTmaTeamThreads * kPwgComputeRegs + 128 * kPwgProducerRegs <= 96 * 640, "setmaxnreg pool");
@@ -59,9 +60,9 @@ struct TmaArgs {
     uint32_t cmask[4];        // coordinate mask of each dimension (span bits)
     int32_t elems0;           // tensor elements per amplitude in dimension 0 (2 for complex128)
     uint32_t wcombo[16];      // last group: TMA-layout byte offset of register j
-    uint32_t wtcol[8];        // last group: TMA-layout byte offset of thread bit m
+    uint32_t wtcol[9];        // last group: TMA-layout byte offset of thread bit m
     uint64_t gwcombo[16];     // last group, direct stores: global amplitude offset of register j
-    uint64_t gwtcol[8];       // last group, direct stores: global amplitude offset of thread bit m
+    uint64_t gwtcol[9];       // last group, direct stores: global amplitude offset of thread bit m
     const unsigned char* base;   // state-slot array (the tensor's base address)
     uint64_t state_bytes;
     uint32_t tile_bytes, mat_bytes;
@@ -169,8 +170,9 @@ __device__ __forceinline__ void bulk_wait_read(int n) {
 }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+template <int TT>
 __device__ __forceinline__ void team_sync(int team) {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "n"(kTmaTeamThreads) : "memory");
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "n"(TT) : "memory");
 }
 
 // TEAMS compute teams of 8 warps each take alternate items (team t: items
@@ -202,8 +204,8 @@ __device__ __forceinline__ void team_sync(int team) {
 // shared-memory loads, stores and barriers run under the other team's math
 // instead of in phase with it (both teams computing at once doubled every
 // group's time, QV_TMA_TRACE).
-template <typename T, int STAGES, int TEAMS, bool DIRECT, bool PWG, bool ALT>
-__global__ void __launch_bounds__(tma_threads(TEAMS, PWG), 1)
+template <typename T, int TBITS, int STAGES, int TEAMS, bool DIRECT, bool PWG, bool ALT>
+__global__ void __launch_bounds__(tma_threads(TEAMS, PWG, TBITS), 1)
 tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, const TmaArgs ta,
                 const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent, int nstates, int64_t ntiles) {
     static_assert(!DIRECT || TEAMS > 1, "direct stores are issued by the teams themselves");
@@ -213,8 +215,9 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     typedef typename Cx<T>::V V;
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
     constexpr int NA = 1 << R;
-    constexpr int TB = 8;
-    constexpr int COMPUTE = TEAMS * kTmaTeamThreads;
+    constexpr int TB = TBITS;
+    constexpr int TT = 1 << TB;   // threads of a team: one register group covers the tile
+    constexpr int COMPUTE = TEAMS * TT;
     extern __shared__ __align__(1024) unsigned char tma_smem[];
     unsigned char* smem_raw = tma_smem;
     const uint32_t TILE = ta.tile_bytes;
@@ -304,10 +307,10 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(full0 + 8 * s, 1);
                 mbar_init(full0 + 8 * (STAGES + s), 1);
-                mbar_init(done0 + 8 * s, kTmaTeamThreads / 32);   // one arrival per warp
+                mbar_init(done0 + 8 * s, TT / 32);   // one arrival per warp
             }
-            mbar_init(tok0, kTmaTeamThreads / 32);
-            mbar_init(tok0 + 8, kTmaTeamThreads / 32);
+            mbar_init(tok0, TT / 32);
+            mbar_init(tok0 + 8, TT / 32);
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             fence_proxy_async_smem();
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
@@ -334,8 +337,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
 
     // ---------------------------------------------------------------- compute
     if constexpr (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPwgComputeRegs) : "memory");
-    const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / kTmaTeamThreads);
-    const int tid = (int)(threadIdx.x % kTmaTeamThreads);
+    const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / TT);
+    const int tid = (int)(threadIdx.x % TT);
     // ALT: math phases of this team so far, and how many each team has in total
     int phase = 0;
     const int phases0 = ((my_items + 1) / 2) * pd.ng, phases1 = (my_items / 2) * pd.ng;
@@ -361,8 +364,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             // so a slow warp of the previous item never sees them change)
             out = sout[s];
             V* tm = reinterpret_cast<V*>(smem_raw + ta.tmat_off + (size_t)(2 * team + ((i / TEAMS) & 1)) * ta.mat_bytes);
-            for (int q = tid; q < pd.nm * 4; q += kTmaTeamThreads) tm[q] = smat[q];
-            team_sync(team);
+            for (int q = tid; q < pd.nm * 4; q += TT) tm[q] = smat[q];
+            team_sync<TT>(team);
             smat = tm;
         }
         for (int g = 0; g < pd.ng; ++g) {
@@ -399,7 +402,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             if (DIRECT && last) {
                 // every thread of the team has read the stage: hand it to the
                 // load of item i + STAGES
-                team_sync(team);
+                team_sync<TT>(team);
                 if (tid == 0 && i + STAGES < my_items) {
                     issue_load(i + STAGES);
                     for (int q = 0; q < ta.pieces; ++q) load_piece(s, q);
@@ -436,7 +439,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 // diagnostic: keep the results live without the smem store
                 if (a[0].x == T(-12345.678)) *reinterpret_cast<V*>(smem_raw + off(0)) = a[1];
                 if (!sg[g + 1].cta_sync) __syncwarp();
-                else team_sync(team);
+                else team_sync<TT>(team);
             } else if (!last) {
                 // re-read the four register-bit columns (volatile: the 16 slot
                 // offsets are recomputed here instead of being held -- or
@@ -448,7 +451,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                     *reinterpret_cast<V*>(smem_raw + (base ^ ((j & 1) ? sc0 : 0u) ^ ((j & 2) ? sc1 : 0u) ^
                                                       ((j & 4) ? sc2 : 0u) ^ ((j & 8) ? sc3 : 0u))) = a[j];
                 if (!sg[g + 1].cta_sync) __syncwarp();
-                else team_sync(team);
+                else team_sync<TT>(team);
             } else if constexpr (DIRECT) {
                 TMA_MARK(i, 12);
 #pragma unroll
@@ -457,7 +460,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             } else {
                 // every thread of the team has read its amplitudes before any
                 // is rewritten in the TMA box layout
-                team_sync(team);
+                team_sync<TT>(team);
 #pragma unroll
                 for (int j = 0; j < NA; ++j)
                     *reinterpret_cast<V*>(smem_raw + (boff ^ wbase ^ ta.wcombo[j])) = a[j];
@@ -469,7 +472,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 __syncwarp();   // the warp's fenced writes, then one arrival per warp
                 if ((tid & 31) == 0) mbar_arrive(done0 + 8 * s);
             } else {
-                team_sync(team);
+                team_sync<TT>(team);
                 TMA_MARK(i, 12);
                 if (tid == 0) turn_stage(s, i + STAGES);
                 TMA_MARK(i, 13);
