@@ -564,6 +564,13 @@ Plan build_plan(const Topology& topo, int precision, int max_tile_bits) {
                 uint32_t row = 0;
                 for (int mm = 0; mm < c && mm < tbits; ++mm) row |= inv[G.tcol[mm] >> shift];
                 tl.coalesced = row == (1u << c) - 1 ? 1 : 0;
+                // first group: physical slot -> initial logical index (the
+                // load layout swz is a permutation under the TMA swizzle)
+                std::vector<uint32_t> inv0((size_t)1 << k);
+                for (uint32_t l = 0; l < (1u << k); ++l) inv0[apply_cols(d.swz, k, l)] = l;
+                const GroupDesc& F = plan.groups[d.g0];
+                for (int mm = 0; mm < tbits && mm < 11; ++mm) tl.flam[mm] = inv0[F.tcol[mm] >> shift];
+                for (int r = 0; r < R; ++r) tl.fmu[r] = inv0[F.combo[1 << r] >> shift];
             }
             tl.wavefronts = wf;
         };

@@ -144,6 +144,12 @@ struct TmaLayout {
     uint64_t gwcombo[16] = {0};
     uint64_t gwtcol[11] = {0};
     int32_t coalesced = 0;      // lanes 0..c-1 of the last group write one contiguous 128-byte row
+    // initial logical tile index of the FIRST group's thread bit m / register
+    // bit r: a register whose index has a `fresh` bit (never touched before
+    // this pass: the amplitude is 0) is zero-filled as it is read, so passes
+    // with fresh bits also run on the TMA kernel (the box still loads them)
+    uint32_t flam[11] = {0};
+    uint32_t fmu[4] = {0};
     int64_t wavefronts = 0;     // bank model of the chosen layout (tools / tests)
 };
 

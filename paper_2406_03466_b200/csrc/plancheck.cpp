@@ -298,6 +298,97 @@ int qvp_simulate_cone(int n, int64_t n_gates, const uint8_t* kinds, const int32_
     }
 }
 
+int qvp_simulate_cone_tma(int n, int64_t n_gates, const uint8_t* kinds, const int32_t* q0, const int32_t* q1,
+                      const double* angles, int precision, int max_tile_bits, const uint64_t* support,
+                      int64_t S, double* out_probs, int64_t* tiles_visited) {
+    try {
+        const Topology topo = make_topo(n, n_gates, kinds, q0, q1);
+        const Plan plan = build_plan(topo, precision, max_tile_bits);
+        if (plan.single_tile) return -1;
+        std::vector<double> mats((size_t)plan.n_slots() * 8);
+        circuit_matrices(plan, topo, angles, mats.data());
+        const LightCone lc = light_cone(plan, support, S);
+        const int R = reg_bits(precision), NA = 1 << R;
+        const int k = plan.k, tb = k - R, nt = 1 << tb;
+        const double nan = std::numeric_limits<double>::quiet_NaN();
+        std::vector<cd> st((size_t)1 << n, cd(nan, nan)), tile((size_t)1 << k);
+        const int sh = precision == 0 ? 4 : 3;
+        int64_t visited = 0;
+        for (size_t p = 0; p < plan.pdesc.size(); ++p) {
+            const PassDesc pd = restrict_pass(plan.pdesc[p], lc.outer_free[p], lc.fresh[p]);
+            const TmaLayout& tl = plan.tma[p];
+            const bool use_tma = p > 0 && tl.ok;
+            const int64_t ntiles = 1ll << pd.n_outer;
+            visited += ntiles;
+            for (int64_t x = 0; x < ntiles; ++x) {
+                uint64_t outer = 0;
+                for (int j = 0; j < pd.n_outer; ++j)
+                    if ((x >> j) & 1) outer |= 1ull << pd.obits[j];
+                for (int tid = 0; tid < nt; ++tid) {
+                    uint32_t ts = 0;
+                    uint64_t tg = 0;
+                    for (int j = 0; j < tb; ++j)
+                        if ((tid >> j) & 1) { ts ^= pd.swz[j]; tg |= 1ull << pd.sbits[j]; }
+                    for (int it = 0; it < NA; ++it) {
+                        const uint32_t local = (uint32_t)tid | ((uint32_t)it << tb);
+                        cd v;
+                        if (p == 0) v = (x == 0 && local == 0) ? cd(1, 0) : cd(0, 0);   // generated |0...0>
+                        else if ((local & pd.fresh) && !use_tma) v = cd(0, 0);
+                        else v = st[outer | tg | pd.g_hi[it]];   // TMA: fresh slots load whatever is there
+                        tile[ts ^ pd.swz_hi[it]] = v;
+                    }
+                }
+                for (int g = pd.g0; g < pd.g0 + pd.ng; ++g) {
+                    const GroupDesc& G = plan.groups[g];
+                    for (int tid = 0; tid < nt; ++tid) {
+                        uint32_t base = 0;
+                        for (int m = 0; m < tb; ++m)
+                            if ((tid >> m) & 1) base ^= G.tcol[m];
+                        cd a[16];
+                        for (int j = 0; j < NA; ++j) a[j] = tile[(base ^ G.combo[j]) >> sh];
+                        if (use_tma && pd.fresh && g == pd.g0) {   // zero-fill fresh registers as read
+                            uint32_t lt = 0;
+                            for (int m = 0; m < tb; ++m)
+                                if ((tid >> m) & 1) lt ^= tl.flam[m];
+                            for (int j = 0; j < NA; ++j) {
+                                uint32_t l = lt;
+                                for (int r = 0; r < R; ++r)
+                                    if ((j >> r) & 1) l ^= tl.fmu[r];
+                                if (l & pd.fresh) a[j] = cd(0, 0);
+                            }
+                        }
+                        for (int r = 0; r < R; ++r) {
+                            if (G.mat[r] < 0) continue;
+                            const double* M = mats.data() + (size_t)(pd.m0 + G.mat[r]) * 8;
+                            const cd m00(M[0], M[1]), m01(M[2], M[3]), m10(M[4], M[5]), m11(M[6], M[7]);
+                            for (int j = 0; j < NA; ++j) {
+                                if ((j >> r) & 1) continue;
+                                const cd u = a[j], v = a[j | (1 << r)];
+                                a[j] = m00 * u + m01 * v;
+                                a[j | (1 << r)] = m10 * u + m11 * v;
+                            }
+                        }
+                        for (int j = 0; j < NA; ++j) tile[(base ^ G.combo[j]) >> sh] = a[j];
+                    }
+                }
+                for (int tid = 0; tid < nt; ++tid) {
+                    uint32_t fs = 0;
+                    uint64_t tg = 0;
+                    for (int j = 0; j < tb; ++j)
+                        if ((tid >> j) & 1) { fs ^= pd.fin[j]; tg |= 1ull << pd.sbits[j]; }
+                    for (int it = 0; it < NA; ++it) st[outer | tg | pd.g_hi[it]] = tile[fs ^ pd.fin_hi[it]];
+                }
+            }
+        }
+        for (int64_t s = 0; s < S; ++s)
+            out_probs[s] = (support[s] & ~lc.reach) ? 0.0 : std::norm(st[support[s]]);
+        if (tiles_visited) *tiles_visited = visited;
+        return (int)plan.pdesc.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // Plan shape: stats[0] passes, [1] groups, [2] matrix slots, [3] fused ops,
 // [4] tile bits, [5] single tile, [6] groups needing a CTA barrier;
 // per-pass matrices in pass_mats (if non-null, <= cap).

@@ -487,7 +487,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
     const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);
     const size_t tma_smem = ent_off + (size_t)nstates * 3 * sizeof(uint64_t);
-    if (tl && tl->ok && arena && arena->base && multi && tb == multi_tile_tb<T>() && ep.flags == F_STORE && pd.fresh == 0 &&
+    if (tl && tl->ok && arena && arena->base && multi && tb == multi_tile_tb<T>() && ep.flags == F_STORE &&
         !generated && pd.ng >= 1 && mat_bytes <= (size_t)kTmaMatBytes && tma_smem <= kTmaSmemCap && tma_enabled() &&
         encode_tiled()) {
         TmaArgs ta;
@@ -537,6 +537,8 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
             ta.wtcol[m] = tl->wtcol[m];
             ta.gwtcol[m] = tl->gwtcol[m];
         }
+        for (int m = 0; m < 9; ++m) ta.flam[m] = tl->flam[m];
+        for (int r = 0; r < 4; ++r) ta.fmu[r] = tl->fmu[r];
         ta.tmat_off = (uint32_t)tmat_off;
         ta.ent_off = (uint32_t)ent_off;
         ta.pieces = pieces;

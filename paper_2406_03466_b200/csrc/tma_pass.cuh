@@ -68,6 +68,8 @@ struct TmaArgs {
     uint32_t tile_bytes, mat_bytes;
     uint32_t tmat_off;        // direct stores: byte offset of the teams' matrix buffers
     uint32_t ent_off;         // byte offset of the launch's (in, out, mats) table in shared memory
+    uint32_t flam[9];         // first group: initial logical tile index of thread bit m
+    uint32_t fmu[4];          // first group: initial logical tile index of register bit r
     int32_t pieces;           // a tile moves as `pieces` boxes split along the outermost box dimension
     int32_t piece_step;       // coordinate step between pieces along dimension ndim - 1
     long long* trace;         // QV_TMA_TRACE builds only (tools/tma_trace.py), else null
@@ -342,12 +344,13 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     // ALT: math phases of this team so far, and how many each team has in total
     int phase = 0;
     const int phases0 = ((my_items + 1) / 2) * pd.ng, phases1 = (my_items / 2) * pd.ng;
-    uint32_t wbase = 0;
+    uint32_t wbase = 0, flt = 0;
     uint64_t gbase = 0;
 #pragma unroll
     for (int m = 0; m < TB; ++m)
         if ((tid >> m) & 1) {
             wbase ^= ta.wtcol[m];
+            flt ^= ta.flam[m];
             if constexpr (DIRECT) gbase ^= ta.gwtcol[m];
         }
     for (int i = team; i < my_items; i += TEAMS) {
@@ -397,6 +400,16 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             } else {
 #pragma unroll
                 for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off(j));
+            }
+            if (g == 0 && pd.fresh) {
+                // slots whose initial index has a bit no earlier pass touched
+                // hold amplitude 0 (the box brought whatever HBM had there)
+#pragma unroll
+                for (int j = 0; j < NA; ++j) {
+                    const uint32_t l = flt ^ ((j & 1) ? ta.fmu[0] : 0u) ^ ((j & 2) ? ta.fmu[1] : 0u) ^
+                                       ((j & 4) ? ta.fmu[2] : 0u) ^ ((j & 8) ? ta.fmu[3] : 0u);
+                    if (l & pd.fresh) a[j] = V{T(0), T(0)};
+                }
             }
             const bool last = g + 1 == pd.ng;
             if (DIRECT && last) {

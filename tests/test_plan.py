@@ -119,8 +119,8 @@ def test_small_register_is_single_tile(plan_lib):
     assert st[5] == 1 and st[0] == 1 and st[4] == 4
 
 
-def _simulate_cone(lib, n, gates, tile_bits, support, precision=0):
-    f = lib.qvp_simulate_cone
+def _simulate_cone(lib, n, gates, tile_bits, support, precision=0, tma=False):
+    f = lib.qvp_simulate_cone_tma if tma else lib.qvp_simulate_cone
     f.restype = ctypes.c_int
     f.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_int,
                                                                             ctypes.c_void_p, ctypes.c_int64,
@@ -155,9 +155,12 @@ def test_light_cone_restriction_reads_only_written_data(plan_lib, seed):
                 np.array([int(rng.integers(0, 1 << n))], np.uint64),
                 np.array([0, (1 << n) - 1], np.uint64)]
     for sup in supports:
-        got, visited, passes = _simulate_cone(plan_lib, n, gates, tile, sup)
-        assert not np.any(np.isnan(got)), sup
-        assert np.max(np.abs(got - probs[sup.astype(np.int64)])) < 1e-12, sup
+        for tma in (False, True):
+            # tma: passes with a TMA layout load their whole box (fresh slots
+            # included, NaN here) and zero the fresh registers on the first read
+            got, visited, passes = _simulate_cone(plan_lib, n, gates, tile, sup, tma=tma)
+            assert not np.any(np.isnan(got)), (sup, tma)
+            assert np.max(np.abs(got - probs[sup.astype(np.int64)])) < 1e-12, (sup, tma)
     # the low-index support sweeps far fewer tiles than the full passes
     _, visited, passes = _simulate_cone(plan_lib, n, gates, tile, supports[0])
     assert visited < passes * (1 << (n - tile))
