@@ -388,8 +388,10 @@ template <typename T>
 TmaFn tma_kernel(int teams, bool direct, bool pwg, bool alt) {
     constexpr int ST = tma_stages<T>();
     constexpr int TBI = multi_tile_tb<T>();
-    if constexpr (TBI != 8) {   // 512-thread tiles: one team + the producer warp
-        return &tma_pass_kernel<T, TBI, ST, 1, false, false, false>;
+    if constexpr (TBI != 8) {   // 8 K-amplitude tiles: one 512-thread team + the producer warp, or two
+                                // 256-thread teams holding two register groups per thread
+        if (teams == 1) return &tma_pass_kernel<T, TBI, ST, 1, false, false, false>;
+        return &tma_pass_kernel<T, TBI, ST, 2, false, false, false>;
     } else {
         if (teams == 1) return &tma_pass_kernel<T, 8, ST, 1, false, false, false>;
         if (direct)
@@ -480,9 +482,9 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const size_t tile_bytes = sizeof(V) << pd.k;
     const size_t mat_bytes = (size_t)pd.nm * 4 * sizeof(V);
     constexpr int ST = tma_stages<T>();
-    const int teams = multi_tile_tb<T>() == 8 ? tma_teams() : 1;
-    const bool direct = teams > 1 && tma_direct();
-    const bool pwg = teams > 1 && !direct && tma_pwg(E.precision);
+    const int teams = tma_teams();
+    const bool direct = teams > 1 && multi_tile_tb<T>() == 8 && tma_direct();
+    const bool pwg = teams > 1 && multi_tile_tb<T>() == 8 && !direct && tma_pwg(E.precision);
     const bool alt = (direct || pwg) && tma_alt();
     const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
     const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);

@@ -46,8 +46,11 @@ constexpr int kTmaTeamThreads = 256;       // 2^(12 - 4): one register group cov
 // 96 registers per thread; the producer warpgroup gives most of its share back
 // (setmaxnreg 24) and the compute warpgroups take 112 -- within the CTA's
 // pool of 96 x 640 (asking for more than the pool holds never returns).
+// Two teams on tiles of 2^tbits register groups, tbits > 8 (complex64, 13-bit
+// tiles): each team keeps 256 threads, every thread holding 2^(tbits - 8)
+// register groups of the tile ("sub-batches").
 __host__ __device__ constexpr int tma_threads(int teams, bool pwg = false, int tbits = 8) {
-    return teams == 1 ? (1 << tbits) + 32 : 2 * (1 << tbits) + (pwg ? 128 : 0);
+    return teams == 1 ? (1 << tbits) + 32 : 2 * (1 << (tbits < 8 ? tbits : 8)) + (pwg ? 128 : 0);
 }
 constexpr int kPwgComputeRegs = 112, kPwgProducerRegs = 24;
 static_assert(2 * kTmaTeamThreads * kPwgComputeRegs + 128 * kPwgProducerRegs <= 96 * 640, "setmaxnreg pool");
@@ -83,6 +86,9 @@ struct TmaArgs {
 constexpr int kTraceCtas = 4, kTraceItems = 64;
 #ifndef QV_TMA_DIAG_NOMATH
 #define QV_TMA_DIAG_NOMATH 0   // diagnostic builds only: skip the 2x2 math (wrong results)
+#endif
+#ifndef QV_TMA_DIAG_NOHBM
+#define QV_TMA_DIAG_NOHBM 0    // diagnostic builds only: no tile loads / stores (wrong results)
 #endif
 #ifdef QV_TMA_TRACE
 #define TMA_MARK(item, ev)                                                                             \
@@ -140,18 +146,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, const int32_t* c, uint32_t bar) {
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, int32_t c0, int32_t c1, int32_t c2,
+                                            int32_t c3, int32_t c4, uint32_t bar) {
     asm volatile(
         "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
-        "l"(tmap), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void tma_store_5d(const void* tmap, const int32_t* c, uint32_t src) {
+__device__ __forceinline__ void tma_store_5d(const void* tmap, int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                             int32_t c4, uint32_t src) {
     asm volatile(
         "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group"
         " [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(tmap),
-        "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(src)
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src)
         : "memory");
 }
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -218,7 +226,13 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
     constexpr int NA = 1 << R;
     constexpr int TB = TBITS;
-    constexpr int TT = 1 << TB;   // threads of a team: one register group covers the tile
+    // threads of a team: with one team, one register group per thread covers
+    // the tile; two teams keep 256 threads and SUB groups per thread
+    constexpr int SUB = (TEAMS == 2 && TB > 8) ? 1 << (TB - 8) : 1;
+    constexpr int TT = (1 << TB) / SUB;
+    constexpr int TTB = TB - (SUB == 2 ? 1 : SUB == 4 ? 2 : 0);   // log2(TT)
+    static_assert(SUB <= 2 && (1 << TTB) == TT, "at most two sub-batches per thread");
+    static_assert(SUB == 1 || (!DIRECT && !PWG && !ALT), "sub-batches: bulk stores by the team");
     constexpr int COMPUTE = TEAMS * TT;
     extern __shared__ __align__(1024) unsigned char tma_smem[];
     unsigned char* smem_raw = tma_smem;
@@ -238,33 +252,51 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     // the item's load, before the arrival that releases them with the tile
     __shared__ int32_t soc[STAGES][5];
     __shared__ V* sout[STAGES];
-    int32_t lc[5];        // load coordinates of the item being issued (issuing thread)
-    uint32_t lbar = 0;    // and its full barrier
-    // the launch's state pointers, staged once: the thread that issues a load
-    // never waits on a global read in the middle of an item
+    int32_t lc0 = 0, lc1 = 0, lc2 = 0, lc3 = 0, lc4 = 0;   // load coordinates of the item being issued
+    uint32_t lbar = 0;                                      // and its full barrier
+    // the launch's per-state constants, staged once (matrix table, output
+    // pointer, input / output state slot): the thread that issues a load
+    // never waits on a global read or divides in the middle of an item
     const uint64_t* sent = reinterpret_cast<const uint64_t*>(smem_raw + ta.ent_off);
+    // Coordinates as five scalars (dimension `ndim` is the state slot):
+    // written out per dimension so nothing is indexed at run time and the
+    // issuing thread never touches local memory.
+    auto coord = [&](int d, uint64_t o, int32_t slot) -> int32_t {
+        int32_t v = d < ta.ndim ? (int32_t)((o >> ta.lo[d & 3]) & ta.cmask[d & 3]) : 0;
+        if (d == 0) v *= ta.elems0;
+        return d == ta.ndim ? slot : v;
+    };
     auto issue_load = [&](int i) {
         const int w = (int)blockIdx.x + i * G;
         const int x = w / nstates, y = w - x * nstates;
-        struct { const void* in; void* out; const void* mats; } e = {
-            reinterpret_cast<const void*>(sent[3 * y]), reinterpret_cast<void*>(sent[3 * y + 1]),
-            reinterpret_cast<const void*>(sent[3 * y + 2])};
+        const void* mats = reinterpret_cast<const void*>(sent[3 * y]);
+        void* out = reinterpret_cast<void*>(sent[3 * y + 1]);
+        const uint64_t slots = sent[3 * y + 2];
+        const int32_t in_slot = (int32_t)(uint32_t)slots, out_slot = (int32_t)(slots >> 32);
         uint64_t o = 0;   // outer offset of tile x (light-cone restricted passes list fewer bits)
         for (int j = 0; j < pd.n_outer; ++j)
             if ((x >> j) & 1) o |= 1ull << pd.obits[j];
         const int s = i % STAGES;
-        int32_t c[5] = {0, 0, 0, 0, 0};
-        for (int d = 0; d < ta.ndim; ++d) c[d] = (int32_t)((o >> ta.lo[d]) & ta.cmask[d]);
-        c[0] *= ta.elems0;
-        for (int d = 0; d < 5; ++d) soc[s][d] = c[d];
-        soc[s][ta.ndim] = (int32_t)(((const unsigned char*)e.out - ta.base) / ta.state_bytes);
-        sout[s] = reinterpret_cast<V*>(e.out) + o;
-        c[ta.ndim] = (int32_t)(((const unsigned char*)e.in - ta.base) / ta.state_bytes);
+        soc[s][0] = coord(0, o, out_slot);
+        soc[s][1] = coord(1, o, out_slot);
+        soc[s][2] = coord(2, o, out_slot);
+        soc[s][3] = coord(3, o, out_slot);
+        soc[s][4] = coord(4, o, out_slot);
+        sout[s] = reinterpret_cast<V*>(out) + o;
+        lc0 = coord(0, o, in_slot);
+        lc1 = coord(1, o, in_slot);
+        lc2 = coord(2, o, in_slot);
+        lc3 = coord(3, o, in_slot);
+        lc4 = coord(4, o, in_slot);
         const uint32_t bar = full0 + 8 * full_of<STAGES>(i);
+        lbar = bar;
+        if (QV_TMA_DIAG_NOHBM) {
+            mbar_arrive(bar);
+            return;
+        }
         mbar_expect_tx(bar, TILE + ta.mat_bytes);
-        bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes, reinterpret_cast<const V*>(e.mats) + (size_t)pd.m0 * 4,
+        bulk_load(sbase + STAGES * TILE + s * kTmaMatBytes, reinterpret_cast<const V*>(mats) + (size_t)pd.m0 * 4,
                   ta.mat_bytes, bar);
-        for (int d = 0; d < 5; ++d) lc[d] = c[d];
         lbar = bar;
     };
     // The tile as `pieces` boxes (split along the outermost box dimension,
@@ -272,15 +304,19 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     // it overlap piece by piece -- piece q of the next item loads as soon as
     // piece q of the last one has been read out.
     const uint32_t PIECE = TILE / (uint32_t)ta.pieces;
+    const int pdim = ta.ndim - 1;   // the dimension pieces step along
     auto load_piece = [&](int s, int q) {
-        int32_t c[5] = {lc[0], lc[1], lc[2], lc[3], lc[4]};
-        c[ta.ndim - 1] += q * ta.piece_step;
-        tma_load_5d(sbase + s * TILE + q * PIECE, &tmap, c, lbar);
+        if (QV_TMA_DIAG_NOHBM) return;
+        const int32_t dq = q * ta.piece_step;
+        tma_load_5d(sbase + s * TILE + q * PIECE, &tmap, lc0 + (pdim == 0 ? dq : 0), lc1 + (pdim == 1 ? dq : 0),
+                    lc2 + (pdim == 2 ? dq : 0), lc3 + (pdim == 3 ? dq : 0), lc4, lbar);
     };
     auto store_piece = [&](int s, int q) {
-        int32_t c[5] = {soc[s][0], soc[s][1], soc[s][2], soc[s][3], soc[s][4]};
-        c[ta.ndim - 1] += q * ta.piece_step;
-        tma_store_5d(&tmap, c, sbase + s * TILE + q * PIECE);
+        if (QV_TMA_DIAG_NOHBM) return;
+        const int32_t dq = q * ta.piece_step;
+        tma_store_5d(&tmap, soc[s][0] + (pdim == 0 ? dq : 0), soc[s][1] + (pdim == 1 ? dq : 0),
+                     soc[s][2] + (pdim == 2 ? dq : 0), soc[s][3] + (pdim == 3 ? dq : 0), soc[s][4],
+                     sbase + s * TILE + q * PIECE);
         bulk_commit();
     };
     // store the item in stage s, then load item `next` (if any) into it
@@ -300,9 +336,11 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         for (int i = threadIdx.x; i < pd.ng * 8; i += blockDim.x) gdst[i] = gsrc[i];
         uint64_t* se = reinterpret_cast<uint64_t*>(smem_raw + ta.ent_off);
         for (int y = threadIdx.x; y < nstates; y += blockDim.x) {
-            se[3 * y] = reinterpret_cast<uint64_t>(ent[y].in);
+            const uint64_t in_slot = (uint64_t)((const unsigned char*)ent[y].in - ta.base) / ta.state_bytes;
+            const uint64_t out_slot = (uint64_t)((const unsigned char*)ent[y].out - ta.base) / ta.state_bytes;
+            se[3 * y] = reinterpret_cast<uint64_t>(ent[y].mats);
             se[3 * y + 1] = reinterpret_cast<uint64_t>(ent[y].out);
-            se[3 * y + 2] = reinterpret_cast<uint64_t>(ent[y].mats);
+            se[3 * y + 2] = (uint32_t)in_slot | (out_slot << 32);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -347,7 +385,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     uint32_t wbase = 0, flt = 0;
     uint64_t gbase = 0;
 #pragma unroll
-    for (int m = 0; m < TB; ++m)
+    for (int m = 0; m < TTB; ++m)
         if ((tid >> m) & 1) {
             wbase ^= ta.wtcol[m];
             flt ^= ta.flam[m];
@@ -381,35 +419,44 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             }
             uint32_t base = boff;
 #pragma unroll
-            for (int m = 0; m < TB; ++m)
+            for (int m = 0; m < TTB; ++m)
                 if ((tid >> m) & 1) base ^= GD.tcol[m];
+            // sub-batch h of this thread: virtual thread tid + h * TT
+            const uint32_t hcol = SUB > 1 ? GD.tcol[TTB < 10 ? TTB : 0] : 0u;
             // slot of register j = base ^ combo[j]; combo is the XOR of the
             // four register-bit columns combo[1], [2], [4], [8]
             const uint4 c0 = reinterpret_cast<const uint4*>(GD.combo)[0];
             const uint32_t rc0 = c0.y, rc1 = c0.z, rc2 = GD.combo[4], rc3 = GD.combo[8];
-            auto off = [&](int j) -> uint32_t {
-                return base ^ ((j & 1) ? rc0 : 0u) ^ ((j & 2) ? rc1 : 0u) ^ ((j & 4) ? rc2 : 0u) ^ ((j & 8) ? rc3 : 0u);
+            auto off = [&](int h, int j) -> uint32_t {
+                return base ^ (h ? hcol : 0u) ^ ((j & 1) ? rc0 : 0u) ^ ((j & 2) ? rc1 : 0u) ^ ((j & 4) ? rc2 : 0u) ^
+                       ((j & 8) ? rc3 : 0u);
             };
-            V a[NA];
+            V a[SUB][NA];
 #ifndef QV_TMA_DIAG_NOSMEM
 #define QV_TMA_DIAG_NOSMEM 0   // diagnostic builds only: registers instead of the group's smem round trip
 #endif
-            if (QV_TMA_DIAG_NOSMEM && g > 0) {
 #pragma unroll
-                for (int j = 0; j < NA; ++j) a[j] = V{T(j + tid), T(g)};
-            } else {
+            for (int h = 0; h < SUB; ++h) {
+                if (QV_TMA_DIAG_NOSMEM && g > 0) {
 #pragma unroll
-                for (int j = 0; j < NA; ++j) a[j] = *reinterpret_cast<const V*>(smem_raw + off(j));
+                    for (int j = 0; j < NA; ++j) a[h][j] = V{T(j + tid), T(g)};
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NA; ++j) a[h][j] = *reinterpret_cast<const V*>(smem_raw + off(h, j));
+                }
             }
             if (g == 0 && pd.fresh) {
                 // slots whose initial index has a bit no earlier pass touched
                 // hold amplitude 0 (the box brought whatever HBM had there)
 #pragma unroll
-                for (int j = 0; j < NA; ++j) {
-                    const uint32_t l = flt ^ ((j & 1) ? ta.fmu[0] : 0u) ^ ((j & 2) ? ta.fmu[1] : 0u) ^
-                                       ((j & 4) ? ta.fmu[2] : 0u) ^ ((j & 8) ? ta.fmu[3] : 0u);
-                    if (l & pd.fresh) a[j] = V{T(0), T(0)};
-                }
+                for (int h = 0; h < SUB; ++h)
+#pragma unroll
+                    for (int j = 0; j < NA; ++j) {
+                        const uint32_t l = flt ^ (h ? ta.flam[TTB < 9 ? TTB : 0] : 0u) ^ ((j & 1) ? ta.fmu[0] : 0u) ^
+                                           ((j & 2) ? ta.fmu[1] : 0u) ^ ((j & 4) ? ta.fmu[2] : 0u) ^
+                                           ((j & 8) ? ta.fmu[3] : 0u);
+                        if (l & pd.fresh) a[h][j] = V{T(0), T(0)};
+                    }
             }
             const bool last = g + 1 == pd.ng;
             if (DIRECT && last) {
@@ -434,8 +481,10 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                         m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
                     }
 #pragma unroll
-                    for (int j = 0; j < NA; ++j)
-                        if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[j], a[j | (1 << r)]);
+                    for (int h = 0; h < SUB; ++h)
+#pragma unroll
+                        for (int j = 0; j < NA; ++j)
+                            if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[h][j], a[h][j | (1 << r)]);
                 }
             }
             if constexpr (ALT) {   // hand the FP64 pipe to the other team
@@ -450,33 +499,40 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             if (g < 10) TMA_MARK(i, 2 + g);
             if (!last && QV_TMA_DIAG_NOSMEM) {
                 // diagnostic: keep the results live without the smem store
-                if (a[0].x == T(-12345.678)) *reinterpret_cast<V*>(smem_raw + off(0)) = a[1];
+                if (a[0][0].x == T(-12345.678)) *reinterpret_cast<V*>(smem_raw + off(0, 0)) = a[0][1];
                 if (!sg[g + 1].cta_sync) __syncwarp();
                 else team_sync<TT>(team);
             } else if (!last) {
-                // re-read the four register-bit columns (volatile: the 16 slot
-                // offsets are recomputed here instead of being held -- or
-                // spilled -- across the group's math)
+                // re-read the register-bit columns (volatile: the slot offsets
+                // are recomputed here instead of being held -- or spilled --
+                // across the group's math)
                 const volatile uint32_t* vc = GD.combo;
                 const uint32_t sc0 = vc[1], sc1 = vc[2], sc2 = vc[4], sc3 = vc[8];
+                const uint32_t sh = SUB > 1 ? reinterpret_cast<const volatile uint32_t*>(GD.tcol)[TTB < 10 ? TTB : 0] : 0u;
 #pragma unroll
-                for (int j = 0; j < NA; ++j)
-                    *reinterpret_cast<V*>(smem_raw + (base ^ ((j & 1) ? sc0 : 0u) ^ ((j & 2) ? sc1 : 0u) ^
-                                                      ((j & 4) ? sc2 : 0u) ^ ((j & 8) ? sc3 : 0u))) = a[j];
+                for (int h = 0; h < SUB; ++h)
+#pragma unroll
+                    for (int j = 0; j < NA; ++j)
+                        *reinterpret_cast<V*>(smem_raw + (base ^ (h ? sh : 0u) ^ ((j & 1) ? sc0 : 0u) ^
+                                                          ((j & 2) ? sc1 : 0u) ^ ((j & 4) ? sc2 : 0u) ^
+                                                          ((j & 8) ? sc3 : 0u))) = a[h][j];
                 if (!sg[g + 1].cta_sync) __syncwarp();
                 else team_sync<TT>(team);
             } else if constexpr (DIRECT) {
                 TMA_MARK(i, 12);
 #pragma unroll
-                for (int j = 0; j < NA; ++j) __stcs(out + (gbase ^ ta.gwcombo[j]), a[j]);
+                for (int j = 0; j < NA; ++j) __stcs(out + (gbase ^ ta.gwcombo[j]), a[0][j]);
                 TMA_MARK(i, 13);
             } else {
                 // every thread of the team has read its amplitudes before any
                 // is rewritten in the TMA box layout
                 team_sync<TT>(team);
 #pragma unroll
-                for (int j = 0; j < NA; ++j)
-                    *reinterpret_cast<V*>(smem_raw + (boff ^ wbase ^ ta.wcombo[j])) = a[j];
+                for (int h = 0; h < SUB; ++h)
+#pragma unroll
+                    for (int j = 0; j < NA; ++j)
+                        *reinterpret_cast<V*>(smem_raw + (boff ^ wbase ^ (h ? ta.wtcol[TTB < 9 ? TTB : 0] : 0u) ^
+                                                          ta.wcombo[j])) = a[h][j];
             }
         }
         if constexpr (!DIRECT) {
