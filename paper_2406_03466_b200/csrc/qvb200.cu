@@ -379,7 +379,7 @@ bool tma_pwg(int precision) {
     return precision == 1;
 }
 // QVB200_TMA_ALT=1: the two teams take turns on the FP64 pipe (producer
-// warpgroup or direct-store kernels only).
+// -- measured).
 bool tma_alt() {
     static const bool a = getenv("QVB200_TMA_ALT") && std::string(getenv("QVB200_TMA_ALT")) == "1";
     return a;
@@ -398,7 +398,7 @@ TmaFn tma_kernel(int teams, bool direct, bool pwg, bool alt) {
             return alt ? &tma_pass_kernel<T, 8, ST, 2, true, false, true> : &tma_pass_kernel<T, 8, ST, 2, true, false, false>;
         if (pwg)
             return alt ? &tma_pass_kernel<T, 8, ST, 2, false, true, true> : &tma_pass_kernel<T, 8, ST, 2, false, true, false>;
-        return &tma_pass_kernel<T, 8, ST, 2, false, false, false>;
+        return alt ? &tma_pass_kernel<T, 8, ST, 2, false, false, true> : &tma_pass_kernel<T, 8, ST, 2, false, false, false>;
     }
 }
 constexpr size_t kTmaSmemCap = 226 * 1024;   // 227 KiB per block less the kernel's static stage table
@@ -485,7 +485,7 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const int teams = tma_teams();
     const bool direct = teams > 1 && multi_tile_tb<T>() == 8 && tma_direct();
     const bool pwg = teams > 1 && multi_tile_tb<T>() == 8 && !direct && tma_pwg(E.precision);
-    const bool alt = (direct || pwg) && tma_alt();
+    const bool alt = teams > 1 && multi_tile_tb<T>() == 8 && tma_alt();
     const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
     const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);
     const size_t tma_smem = ent_off + (size_t)nstates * 3 * sizeof(uint64_t);

@@ -220,7 +220,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 const GroupDesc* __restrict__ gdesc, const LaunchEntry* __restrict__ ent, int nstates, int64_t ntiles) {
     static_assert(!DIRECT || TEAMS > 1, "direct stores are issued by the teams themselves");
     static_assert(!PWG || (TEAMS == 2 && !DIRECT), "the producer warpgroup serves two teams with bulk stores");
-    static_assert(!ALT || PWG || DIRECT, "alternating math needs teams that never wait on the TMA");
+    static_assert(!ALT || TEAMS == 2, "alternating math needs two teams");
     constexpr bool PRODUCER_THREAD = TEAMS == 1 || PWG;   // a thread outside the teams stores and reloads stages
     typedef typename Cx<T>::V V;
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
