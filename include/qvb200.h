@@ -61,6 +61,9 @@ extern "C" {
 #define QV_OUT_FULL 2       /* per circuit: all 2^n normalised probabilities (n <= 24)          */
 #define QV_OUT_JS 3         /* per circuit: JS(target || p) via the support+remainder identity  */
                             /* (ddcl.py:37-61 over born_distribution)                            */
+#define QV_RES_TARGET_ROWS 1 /* QV_OUT_JS: `target` holds one row of support_count probabilities   */
+                            /* per circuit (circuit c at target + c * support_count), e.g. the   */
+                            /* per-data-point targets of a QCL forward batch (ddcl.py:147-157)   */
 #define QV_OUT_COUNTS 4     /* per circuit: `shots` samples of the outcome distribution with the  */
                             /* reference's sampler (backend.py:140-157): numpy PCG64 doubles,     */
                             /* inverse CDF on the sequential cumsum, side="right" (n <= 24)       */
@@ -90,7 +93,7 @@ typedef struct qv_circuits {
 /* What to return for each circuit. */
 typedef struct qv_results {
     int32_t kind;                  /* QV_OUT_* */
-    int32_t reserved;
+    int32_t flags;                 /* QV_RES_* (0 before this field was defined) */
     /* QV_OUT_PAULI: circuit c owns terms [term_offsets[c], term_offsets[c+1]);
      * a term is a Pauli product given by qubit-bit masks (bit n-1-q for qubit q),
      * exactly the (xmask, ymask, zmask) of backend.py:104-119.                 */
@@ -166,7 +169,10 @@ int64_t qv_last_error_circuit(qv_handle handle);
  * (CUDA events on the executor stream), [6] passes per circuit, [7] tile bits k,
  * [8] device ms of the call (first to last kernel), [9] host->device bytes,
  * [10] device->host bytes, [11] algorithmic flops of pass kernels
- * (28 per amplitude pair per fused 2x2 matrix). */
+ * (28 per amplitude pair per fused 2x2 matrix), [12] TMA pass launches,
+ * [13] read-only Pauli sweeps, [14] / [15] device ms / bytes of TMA passes,
+ * [16] host wall ms of the whole call, [17] host wall ms before its first
+ * kernel (validation, fusion, dedup, planning, copies).  n_stats <= 18. */
 int qv_last_stats(qv_handle handle, double* stats, int32_t n_stats);
 
 /* Library version string, e.g. "qvb200 0.1 sm_100a". */

@@ -318,6 +318,23 @@ class B200Backend:
         self.gate_counter += _gate_count(circuits)
         return flat.reshape(len(circuits), sup.size + 1)[:, : sup.size]
 
+    def js_losses_targets(self, circuits: Sequence[Circuit], n_qubits: int, support, targets: np.ndarray) -> np.ndarray:
+        """JS(targets[c] || P_c) for each circuit against its OWN target row
+        (config 3's forward batch: one target per data point), float64
+        [len(circuits)].  `targets` is [len(circuits), len(support)] in the
+        support's ascending index order; the losses are formed on the device
+        from the support + remainder identity (ddcl.py:37-61), so only one
+        scalar per circuit comes back."""
+        self._check_all(circuits, n_qubits)
+        sup = support_indices(support, n_qubits)
+        t = np.ascontiguousarray(targets, dtype=np.float64)
+        if t.shape != (len(circuits), sup.size):
+            raise ValueError(f"expected targets of shape ({len(circuits)}, {sup.size}), got {t.shape}")
+        out = self._run(lower_batch(circuits), n_qubits, native.QV_OUT_JS, circuits, support=sup, target=t,
+                        flags=native.QV_RES_TARGET_ROWS)
+        self.gate_counter += _gate_count(circuits)
+        return out[: len(circuits)]
+
     def js_losses_rows(self, template: Circuit, values: np.ndarray, target: Mapping[str, float],
                        name_of: Callable[[int], str] | None = None) -> np.ndarray:
         """`js_losses` of the template bound to each parameter row of `values`

@@ -557,6 +557,25 @@ __global__ void finalize_dist_kernel(const int64_t* __restrict__ slots, int64_t 
     }
 }
 
+// Per-circuit targets (QV_RES_TARGET_ROWS): one CTA per circuit, its unique
+// state's normalised support row against its own target row, summed in the
+// order finalize_dist_kernel uses (the same loss for equal targets).
+__global__ void js_rows_kernel(const double* __restrict__ sup_out, const int64_t* __restrict__ urow,
+                               const double* __restrict__ trows, int64_t S, double* __restrict__ js) {
+    __shared__ double sred[32];
+    const double* row = sup_out + urow[blockIdx.x] * (S + 1);
+    const double* t = trows + (int64_t)blockIdx.x * S;
+    double jsum = 0.0, qsum = 0.0;
+    for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
+        const double q = row[s];
+        jsum += js_term(t[s], q);
+        qsum += q;
+    }
+    const double J = block_sum(jsum, sred);
+    const double Q = block_sum(qsum, sred);
+    if (threadIdx.x == 0) js[blockIdx.x] = J + 0.5 * 0.69314718055994530942 * (1.0 - Q);
+}
+
 // Shift-pair finalisation: one CTA per shifted gate.  With A = sum|Psi0|^2,
 // B = sum|Xi|^2, C = sum Im(Psi0 conj Xi), the two shifted distributions are
 // q+-(s) = (a_s + b_s -+ 2 c_s) / (A + B -+ 2 C)  (psi+- = (Psi0 -+ i Xi)/sqrt2),

@@ -14,6 +14,7 @@
 // arithmetic each circuit sees is exactly what it would see alone, so results
 // stay bitwise independent of batch composition and device (pool.py:10-14),
 // while the number of HBM sweeps drops to sum_c (P - branch_pass_c).
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -80,9 +81,19 @@ struct CachedPlan {
 };
 
 
+// Hash of a matrix table, 8 bytes a step (candidates are confirmed with
+// memcmp, so only the spread matters; byte-wise FNV cost ~10 ms per 1 024
+// circuits of 20q x 6L).
 uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
     const unsigned char* p = static_cast<const unsigned char*>(data);
-    for (size_t i = 0; i < bytes; ++i) { h ^= p[i]; h *= 1099511628211ull; }
+    size_t i = 0;
+    for (; i + 8 <= bytes; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, p + i, 8);
+        h = (h ^ w) * 0x9e3779b97f4a7c15ull;
+        h ^= h >> 29;
+    }
+    for (; i < bytes; ++i) { h ^= p[i]; h *= 1099511628211ull; }
     return h;
 }
 
@@ -94,7 +105,11 @@ struct Engine {
     std::mutex mu;
     std::string err;
     int64_t err_circuit = -1;
-    double stats[16] = {0};
+    double stats[18] = {0};   // [16] host ms of the call, [17] host ms before the first launch
+    std::chrono::steady_clock::time_point t_entry;
+    double host_ms() const {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
+    }
     std::unordered_map<std::string, std::unique_ptr<CachedPlan>> plans;
 
     DevBuf<unsigned char> d_states;
@@ -257,8 +272,10 @@ void validate(const Request& q) {
             }
         }
     } else if (r->kind == QV_OUT_SUPPORT || r->kind == QV_OUT_JS) {
+        if (r->flags & ~QV_RES_TARGET_ROWS) throw ArgError("unknown result flags");
         if (r->support_count < 0 || (r->support_count > 0 && !r->support)) throw ArgError("bad support");
         if (r->kind == QV_OUT_JS && r->support_count > 0 && !r->target) throw ArgError("JS needs target probabilities");
+        if ((r->flags & QV_RES_TARGET_ROWS) && r->kind != QV_OUT_JS) throw ArgError("target rows are a JS option");
         for (int64_t s = 0; s < r->support_count; ++s) {
             if (r->support[s] & ~full) throw ArgError("support index beyond the register");
             if (s && r->support[s] <= r->support[s - 1]) throw ArgError("support must be sorted and unique");
@@ -284,9 +301,11 @@ int64_t output_size(const qv_circuits* c, const qv_results* r) {
 }
 
 template <typename F>
-void parallel_for(int64_t count, F fn) {
+void parallel_for(int64_t count, int64_t grain, F fn) {
+    // a thread per `grain` items at most: spawning costs ~20 us a thread, more
+    // than a small batch's whole fusion
     const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
-    const int64_t nthr = std::min<int64_t>(std::min<int64_t>(hw, 16), std::max<int64_t>(1, count / 16));
+    const int64_t nthr = std::min<int64_t>(std::min<int64_t>(hw, 16), std::max<int64_t>(1, count / std::max<int64_t>(1, grain)));
     if (nthr <= 1) { for (int64_t i = 0; i < count; ++i) fn(i); return; }
     std::vector<std::thread> th;
     std::atomic<int64_t> next(0);
@@ -673,11 +692,14 @@ void GroupRun::run() {
     const int slots = plan.n_slots();
     slots8 = (size_t)slots * 8;
     const qv_results* R = q.r;
+    const bool rows = R->kind == QV_OUT_JS && (R->flags & QV_RES_TARGET_ROWS);
     const int P = (int)plan.pdesc.size();
 
     // 1. fused matrices per circuit (host, FP64)
     hmats.assign((size_t)C * slots8, 0.0);
-    parallel_for(C, [&](int64_t i) {
+    // ~1 ns per gate: one thread per >= 64 K gates of fusion work
+    const int64_t gates = std::max<int64_t>(1, (int64_t)topo.kind.size());
+    parallel_for(C, std::max<int64_t>(8, 65536 / gates), [&](int64_t i) {
         double* m = hmats.data() + (size_t)i * slots8;
         circuit_matrices(plan, topo, angle_rows[i], m);
         for (int sl = 0; sl < slots; ++sl) normalise_phase(m + (size_t)sl * 8);
@@ -754,14 +776,33 @@ void GroupRun::run() {
         uint64_t* dsu = E.d_support.get(ep.S);
         h2d(E, dsu, R->support, ep.S * 8);
         ep.support = dsu;
-        if (R->kind == QV_OUT_JS) {
+        if (R->kind == QV_OUT_JS && !rows) {
             double* dta = E.d_target.get(ep.S);
             h2d(E, dta, R->target, ep.S * 8);
             ep.target = dta;
         }
     }
+    // QV_RES_TARGET_ROWS: circuit i's own target row and its unique state's
+    // support row; the losses are formed after the last pass (js_rows_kernel)
+    double* d_trows = nullptr;
+    int64_t* d_urow = nullptr;
+    if (rows && ep.S > 0) {
+        d_trows = E.d_target.get((size_t)C * ep.S);
+        bool contiguous = true;
+        for (int64_t i = 1; i < C && contiguous; ++i) contiguous = circuits[i] == circuits[0] + i;
+        if (contiguous) {
+            h2d(E, d_trows, R->target + (size_t)circuits[0] * ep.S, (size_t)C * ep.S * 8);
+        } else {
+            std::vector<double> t((size_t)C * ep.S);
+            for (int64_t i = 0; i < C; ++i)
+                std::memcpy(t.data() + (size_t)i * ep.S, R->target + (size_t)circuits[i] * ep.S, ep.S * 8);
+            h2d(E, d_trows, t.data(), t.size() * 8);
+        }
+        d_urow = E.d_term_off.get(std::max<int64_t>(1, C));
+        h2d(E, d_urow, uniq_of.data(), C * 8);
+    }
     ep.sup_out = E.d_sup_out.get((size_t)U * (ep.S + 1));
-    ep.js_out = E.d_js_out.get(U);
+    ep.js_out = E.d_js_out.get(rows ? std::max(U, C) : U);
     // full distributions (FULL) and the CDF rows counts mode samples from (COUNTS)
     const bool probs = R->kind == QV_OUT_FULL || R->kind == QV_OUT_COUNTS;
     if (probs) ep.full_out = E.d_full_out.get((size_t)U << n);
@@ -769,6 +810,7 @@ void GroupRun::run() {
     const size_t state_bytes = sizeof(V) << n;
     cudaEvent_t call0 = E.next_event();
     CK(cudaEventRecord(call0, E.stream));
+    if (E.stats[17] == 0.0) E.stats[17] = E.host_ms();
 
     if (plan.single_tile) {
         // whole register in one CTA's shared memory: one launch for the batch
@@ -778,8 +820,8 @@ void GroupRun::run() {
         h2d(E, dent, ents.data(), U * sizeof(LaunchEntry));
         ep.flags = F_SINGLE;
         if (R->kind == QV_OUT_PAULI) ep.flags |= F_S_PAULI;
-        if (R->kind == QV_OUT_SUPPORT) ep.flags |= F_S_SUPPORT;
-        if (R->kind == QV_OUT_JS) ep.flags |= F_S_JS;
+        if (R->kind == QV_OUT_SUPPORT || rows) ep.flags |= F_S_SUPPORT;
+        if (R->kind == QV_OUT_JS && !rows) ep.flags |= F_S_JS;
         if (probs) ep.flags |= F_S_FULL;
         ep.ntiles = 1;
         if (U > 0x7fffffffll) throw ArgError("batch too large");
@@ -1054,7 +1096,7 @@ void GroupRun::run() {
                 E.stats[1] += l.count;
             } else if (l.kind == L_FINAL_DIST) {
                 finalize_dist_kernel<<<l.count, 1024, 0, E.stream>>>(dslots + l.off, rtiles[P - 1], partial, ep.sup_out,
-                                                                     ep.S, ep.target, ep.js_out, R->kind == QV_OUT_JS,
+                                                                     ep.S, ep.target, ep.js_out, R->kind == QV_OUT_JS && !rows,
                                                                      unit_norm);
                 CK(cudaGetLastError());
                 E.stats[0] += 1;
@@ -1117,6 +1159,13 @@ void GroupRun::run() {
             E.stats[0] += 2;
         }
     }
+    double* d_jsrows = nullptr;
+    if (rows && ep.S > 0) {
+        d_jsrows = ep.js_out;
+        js_rows_kernel<<<(unsigned)C, 1024, 0, E.stream>>>(ep.sup_out, d_urow, d_trows, ep.S, d_jsrows);
+        CK(cudaGetLastError());
+        E.stats[0] += 1;
+    }
     cudaEvent_t call1 = E.next_event();
     CK(cudaEventRecord(call1, E.stream));
 
@@ -1135,6 +1184,10 @@ void GroupRun::run() {
         d2h(E, vals.data(), ep.sup_out, vals.size() * 8);
         for (int64_t i = 0; i < C; ++i)
             std::memcpy(out + (size_t)circuits[i] * row, vals.data() + (size_t)uniq_of[i] * row, row * 8);
+    } else if (R->kind == QV_OUT_JS && rows) {
+        std::vector<double> vals(C);
+        if (ep.S > 0) d2h(E, vals.data(), d_jsrows, C * 8);
+        for (int64_t i = 0; i < C; ++i) out[circuits[i]] = vals[i];
     } else if (R->kind == QV_OUT_JS) {
         std::vector<double> vals(U);
         d2h(E, vals.data(), ep.js_out, U * 8);
@@ -1178,6 +1231,7 @@ void execute(Engine& E, const qv_circuits* c, const qv_results* r, double* out, 
     if (need < 0 || out_len < need) throw ArgError("output buffer too small: need " + std::to_string(need));
     CK(cudaSetDevice(E.device));
     std::memset(E.stats, 0, sizeof(E.stats));
+    E.t_entry = std::chrono::steady_clock::now();
     E.events_used = 0;
     CK(cudaStreamSynchronize(E.stream));   // an earlier failed call may have copies in flight
     E.pinned_used = 0;
@@ -1397,6 +1451,7 @@ void run_shift_pairs(Engine& E, CachedPlan& cp, const double* angles, int64_t ns
     if (!slots_tab.empty()) h2d(E, dslots, slots_tab.data(), slots_tab.size() * 8);
     cudaEvent_t call0 = E.next_event();
     CK(cudaEventRecord(call0, E.stream));
+    if (E.stats[17] == 0.0) E.stats[17] = E.host_ms();
     for (const L& l : sched) {
         if (l.pass) {
             EpiArgs e2 = ep;
@@ -1433,6 +1488,7 @@ void shift_js(Engine& E, const qv_circuits* c, int64_t nshift, const int64_t* ga
     validate(q);
     CK(cudaSetDevice(E.device));
     std::memset(E.stats, 0, sizeof(E.stats));
+    E.t_entry = std::chrono::steady_clock::now();
     E.events_used = 0;
     CK(cudaStreamSynchronize(E.stream));   // an earlier failed call may have copies in flight
     E.pinned_used = 0;
@@ -1536,6 +1592,7 @@ int qv_execute(qv_handle h, const qv_circuits* circuits, const qv_results* resul
     E->err_circuit = -1;
     try {
         execute(*E, circuits, results, out, out_len);
+        E->stats[16] = E->host_ms();
         return QV_OK;
     } catch (const CircuitError& e) {
         E->err = e.what();
@@ -1562,6 +1619,7 @@ int qv_shift_js(qv_handle h, const qv_circuits* base, int64_t n_shift, const int
     E->err_circuit = -1;
     try {
         shift_js(*E, base, n_shift, gate_index, results, out);
+        E->stats[16] = E->host_ms();
         return QV_OK;
     } catch (const CircuitError& e) {
         E->err = e.what();
@@ -1601,7 +1659,7 @@ int qv_last_stats(qv_handle h, double* stats, int32_t n_stats) {
     if (!h || !stats) return QV_ERR_ARGUMENT;
     Engine* E = reinterpret_cast<Engine*>(h);
     std::lock_guard<std::mutex> lk(E->mu);
-    for (int i = 0; i < n_stats && i < 16; ++i) stats[i] = E->stats[i];
+    for (int i = 0; i < n_stats && i < 18; ++i) stats[i] = E->stats[i];
     return QV_OK;
 }
 

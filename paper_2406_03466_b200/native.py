@@ -23,6 +23,7 @@ LIB_PATH = Path(os.environ.get("QVB200_LIB") or Path(__file__).resolve().parent 
 QV_OK, QV_ERR_ARGUMENT, QV_ERR_CIRCUIT, QV_ERR_CUDA, QV_ERR_INTERNAL = range(5)
 QV_COMPLEX128, QV_COMPLEX64 = 0, 1
 QV_OUT_PAULI, QV_OUT_SUPPORT, QV_OUT_FULL, QV_OUT_JS, QV_OUT_COUNTS = range(5)
+QV_RES_TARGET_ROWS = 1
 
 PRECISIONS = {"complex128": QV_COMPLEX128, "complex64": QV_COMPLEX64}
 
@@ -32,7 +33,7 @@ EXPORTS = ("qv_version", "qv_output_size", "qv_create", "qv_destroy", "qv_execut
 
 STAT_NAMES = ("launches", "sweeps", "sweeps_unshared", "unique_states", "pass_bytes",
               "pass_ms", "passes_per_circuit", "tile_bits", "device_ms", "h2d_bytes", "d2h_bytes",
-              "pass_flops", "tma_launches", "pauli_state_reads", "tma_ms", "tma_bytes")
+              "pass_flops", "tma_launches", "pauli_state_reads", "tma_ms", "tma_bytes", "host_ms", "host_prep_ms")
 
 
 class NativeUnavailable(RuntimeError):
@@ -54,7 +55,7 @@ class QvCircuits(ctypes.Structure):
 
 
 class QvResults(ctypes.Structure):
-    _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("term_offsets", ctypes.c_void_p),
+    _fields_ = [("kind", ctypes.c_int32), ("flags", ctypes.c_int32), ("term_offsets", ctypes.c_void_p),
                 ("xmask", ctypes.c_void_p), ("ymask", ctypes.c_void_p), ("zmask", ctypes.c_void_p),
                 ("support_count", ctypes.c_int64), ("support", ctypes.c_void_p), ("target", ctypes.c_void_p),
                 ("shots", ctypes.c_int64), ("rng_state", ctypes.c_void_p)]
@@ -138,7 +139,7 @@ class Engine:
     def execute(self, n_qubits: int, lowered: "LoweredBatch", result_kind: int, *,
                 terms: tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray] | None = None,
                 support: np.ndarray | None = None, target: np.ndarray | None = None,
-                shots: int = 0, rng_state: np.ndarray | None = None) -> np.ndarray:
+                shots: int = 0, rng_state: np.ndarray | None = None, flags: int = 0) -> np.ndarray:
         """Run one batch; returns the flat float64 output (layout: qvb200.h)."""
         c = QvCircuits()
         c.n_qubits = n_qubits
@@ -152,6 +153,7 @@ class Engine:
         c.angles = _ptr(lowered.angles)
         r = QvResults()
         r.kind = result_kind
+        r.flags = int(flags)
         keep = []
         if terms is not None:
             off, xm, ym, zm = (np.ascontiguousarray(a) for a in terms)

@@ -260,6 +260,31 @@ def test_forward_losses_batch_of_points(gpu, golden_large):
     assert np.max(np.abs(batch - np.asarray(single))) < 1e-13
 
 
+@pytest.mark.parametrize("n", [8, 14])
+def test_js_losses_against_own_targets(gpu, n):
+    """QV_RES_TARGET_ROWS: each circuit against its own target row equals
+    `js_losses` of that circuit alone with that target -- incl. duplicate
+    circuits (one unique state, two targets) and a batch of two topologies
+    (non-contiguous rows per topology group)."""
+    backend = qv.B200Backend(device=0)
+    layers = 2
+    specs = [qv.DdclSpec(n, layers, qv.random_angles(qv.ddcl_parameter_count(n, layers), 30 + i),
+                         qv.random_target_distribution(n, 40 + i)) for i in range(4)]
+    circuits = [qv.ddcl_circuit(s) for s in specs]
+    circuits.append(qv.ddcl_circuit(specs[0]))   # duplicate state, other target below
+    other = qv.Circuit(n, tuple([qv.h(0)] + [qv.cnot(q, q + 1) for q in range(n - 1)]), name="ghz")
+    circuits.insert(2, other)
+    targets = [s.target for s in specs[:2]] + [specs[3].target] + [s.target for s in specs[2:]] + [specs[1].target]
+    keys = sorted(targets[0])
+    rows = np.asarray([[t[k] for k in keys] for t in targets])
+    got = backend.js_losses_targets(circuits, n, keys, rows)
+    want = [backend.js_losses([c], n, t)[0] for c, t in zip(circuits, targets)]
+    assert np.max(np.abs(got - np.asarray(want))) < 1e-13
+    assert got[0] != got[-1]   # same state, different targets
+    with pytest.raises(ValueError):
+        backend.js_losses_targets(circuits, n, keys, rows[:-1])
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_random_multi_tile_circuits_fuzz(gpu, seed):
     """Random circuits on 13-18 qubits (several tiles, all gate kinds incl.
