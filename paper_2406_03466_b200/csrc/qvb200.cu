@@ -505,7 +505,8 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
     const bool direct = teams > 1 && multi_tile_tb<T>() == 8 && tma_direct();
     const bool pwg = teams > 1 && multi_tile_tb<T>() == 8 && !direct && tma_pwg(E.precision);
     const bool alt = teams > 1 && multi_tile_tb<T>() == 8 && tma_alt();
-    const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng) + 127) & ~(size_t)127;
+    const int team_threads = teams == 1 ? (1 << multi_tile_tb<T>()) : 256;
+    const size_t tmat_off = (TmaSmem<ST>::bytes((uint32_t)tile_bytes, pd.ng, team_threads) + 127) & ~(size_t)127;
     const size_t ent_off = tmat_off + (direct ? 4 * mat_bytes : 0);
     const size_t tma_smem = ent_off + (size_t)nstates * 3 * sizeof(uint64_t);
     if (tl && tl->ok && arena && arena->base && multi && tb == multi_tile_tb<T>() && ep.flags == F_STORE &&

@@ -111,7 +111,11 @@ struct TmaSmem {   // byte offsets inside dynamic shared memory
     __host__ __device__ static constexpr uint32_t done(uint32_t tile) { return full(tile) + 16 * STAGES; }
     __host__ __device__ static constexpr uint32_t tok(uint32_t tile) { return done(tile) + 8 * STAGES; }
     __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return (tok(tile) + 16 + 127) & ~127u; }
-    __host__ __device__ static constexpr uint32_t bytes(uint32_t tile, int ng) { return groups(tile) + 128u * ng; }
+    // per group, each team thread's slot base (XOR of its thread-bit columns)
+    __host__ __device__ static constexpr uint32_t bases(uint32_t tile, int ng) { return groups(tile) + 128u * ng; }
+    __host__ __device__ static constexpr uint32_t bytes(uint32_t tile, int ng, int team_threads) {
+        return bases(tile, ng) + 4u * team_threads * ng;
+    }
 };
 // Item i's tile lands on full barrier full_of(i) = (stage, (i / STAGES) mod 2)
 // and completes its phase full_parity(i).  Two barriers per stage: the items
@@ -343,6 +347,16 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             se[3 * y + 2] = (uint32_t)in_slot | (out_slot << 32);
         }
         __syncthreads();
+        // slot bases of every group for each team thread (one conflict-free
+        // LDS per group instead of TTB descriptor reads and XORs)
+        uint32_t* sb = reinterpret_cast<uint32_t*>(smem_raw + TmaSmem<STAGES>::bases(TILE, pd.ng));
+        for (int j = threadIdx.x; j < pd.ng * TT; j += blockDim.x) {
+            const int g = j / TT, t = j % TT;
+            uint32_t b = 0;
+            for (int m = 0; m < TTB; ++m)
+                if ((t >> m) & 1) b ^= sg[g].tcol[m];
+            sb[j] = b;
+        }
         if (threadIdx.x == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(full0 + 8 * s, 1);
@@ -391,6 +405,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             flt ^= ta.flam[m];
             if constexpr (DIRECT) gbase ^= ta.gwtcol[m];
         }
+    const uint32_t* sbases = reinterpret_cast<const uint32_t*>(smem_raw + TmaSmem<STAGES>::bases(TILE, pd.ng));
     for (int i = team; i < my_items; i += TEAMS) {
         const int s = i % STAGES;
         TMA_MARK(i, 0);
@@ -417,10 +432,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 const V* M = smat + mats.x * 4;
                 m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
             }
-            uint32_t base = boff;
-#pragma unroll
-            for (int m = 0; m < TTB; ++m)
-                if ((tid >> m) & 1) base ^= GD.tcol[m];
+            const uint32_t base = boff ^ sbases[g * TT + tid];
             // sub-batch h of this thread: virtual thread tid + h * TT
             const uint32_t hcol = SUB > 1 ? GD.tcol[TTB < 10 ? TTB : 0] : 0u;
             // slot of register j = base ^ combo[j]; combo is the XOR of the
@@ -459,6 +471,9 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                     }
             }
             const bool last = g + 1 == pd.ng;
+            // read before the math: after the group's 16 shared stores this
+            // load would wait behind them in the MIO queue
+            const bool next_cta_sync = !last && sg[g + 1].cta_sync;
             if (DIRECT && last) {
                 // every thread of the team has read the stage: hand it to the
                 // load of item i + STAGES
@@ -500,7 +515,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             if (!last && QV_TMA_DIAG_NOSMEM) {
                 // diagnostic: keep the results live without the smem store
                 if (a[0][0].x == T(-12345.678)) *reinterpret_cast<V*>(smem_raw + off(0, 0)) = a[0][1];
-                if (!sg[g + 1].cta_sync) __syncwarp();
+                if (!next_cta_sync) __syncwarp();
                 else team_sync<TT>(team);
             } else if (!last) {
                 // re-read the register-bit columns (volatile: the slot offsets
@@ -516,7 +531,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                         *reinterpret_cast<V*>(smem_raw + (base ^ (h ? sh : 0u) ^ ((j & 1) ? sc0 : 0u) ^
                                                           ((j & 2) ? sc1 : 0u) ^ ((j & 4) ? sc2 : 0u) ^
                                                           ((j & 8) ? sc3 : 0u))) = a[h][j];
-                if (!sg[g + 1].cta_sync) __syncwarp();
+                if (!next_cta_sync) __syncwarp();
                 else team_sync<TT>(team);
             } else if constexpr (DIRECT) {
                 TMA_MARK(i, 12);
