@@ -113,8 +113,12 @@ struct TmaSmem {   // byte offsets inside dynamic shared memory
     __host__ __device__ static constexpr uint32_t groups(uint32_t tile) { return (tok(tile) + 16 + 127) & ~127u; }
     // per group, each team thread's slot base (XOR of its thread-bit columns)
     __host__ __device__ static constexpr uint32_t bases(uint32_t tile, int ng) { return groups(tile) + 128u * ng; }
-    __host__ __device__ static constexpr uint32_t bytes(uint32_t tile, int ng, int team_threads) {
+    // per group, its four register-bit columns (combo[1], [2], [4], [8])
+    __host__ __device__ static constexpr uint32_t rcols(uint32_t tile, int ng, int team_threads) {
         return bases(tile, ng) + 4u * team_threads * ng;
+    }
+    __host__ __device__ static constexpr uint32_t bytes(uint32_t tile, int ng, int team_threads) {
+        return rcols(tile, ng, team_threads) + 16u * ng;
     }
 };
 // Item i's tile lands on full barrier full_of(i) = (stage, (i / STAGES) mod 2)
@@ -357,6 +361,9 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 if ((t >> m) & 1) b ^= sg[g].tcol[m];
             sb[j] = b;
         }
+        uint4* sr = reinterpret_cast<uint4*>(smem_raw + TmaSmem<STAGES>::rcols(TILE, pd.ng, TT));
+        for (int g = threadIdx.x; g < pd.ng; g += blockDim.x)
+            sr[g] = make_uint4(sg[g].combo[1], sg[g].combo[2], sg[g].combo[4], sg[g].combo[8]);
         if (threadIdx.x == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(full0 + 8 * s, 1);
@@ -406,6 +413,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             if constexpr (DIRECT) gbase ^= ta.gwtcol[m];
         }
     const uint32_t* sbases = reinterpret_cast<const uint32_t*>(smem_raw + TmaSmem<STAGES>::bases(TILE, pd.ng));
+    const uint4* srcols = reinterpret_cast<const uint4*>(smem_raw + TmaSmem<STAGES>::rcols(TILE, pd.ng, TT));
     for (int i = team; i < my_items; i += TEAMS) {
         const int s = i % STAGES;
         TMA_MARK(i, 0);
@@ -437,8 +445,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             const uint32_t hcol = SUB > 1 ? GD.tcol[TTB < 10 ? TTB : 0] : 0u;
             // slot of register j = base ^ combo[j]; combo is the XOR of the
             // four register-bit columns combo[1], [2], [4], [8]
-            const uint4 c0 = reinterpret_cast<const uint4*>(GD.combo)[0];
-            const uint32_t rc0 = c0.y, rc1 = c0.z, rc2 = GD.combo[4], rc3 = GD.combo[8];
+            const uint4 rcv = srcols[g];
+            const uint32_t rc0 = rcv.x, rc1 = rcv.y, rc2 = rcv.z, rc3 = rcv.w;
             auto off = [&](int h, int j) -> uint32_t {
                 return base ^ (h ? hcol : 0u) ^ ((j & 1) ? rc0 : 0u) ^ ((j & 2) ? rc1 : 0u) ^ ((j & 4) ? rc2 : 0u) ^
                        ((j & 8) ? rc3 : 0u);
@@ -521,8 +529,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 // re-read the register-bit columns (volatile: the slot offsets
                 // are recomputed here instead of being held -- or spilled --
                 // across the group's math)
-                const volatile uint32_t* vc = GD.combo;
-                const uint32_t sc0 = vc[1], sc1 = vc[2], sc2 = vc[4], sc3 = vc[8];
+                const volatile uint4* vc = srcols + g;
+                const uint32_t sc0 = vc->x, sc1 = vc->y, sc2 = vc->z, sc3 = vc->w;
                 const uint32_t sh = SUB > 1 ? reinterpret_cast<const volatile uint32_t*>(GD.tcol)[TTB < 10 ? TTB : 0] : 0u;
 #pragma unroll
                 for (int h = 0; h < SUB; ++h)
