@@ -698,12 +698,32 @@ void GroupRun::run() {
 
     // 1. fused matrices per circuit (host, FP64)
     hmats.assign((size_t)C * slots8, 0.0);
-    // ~1 ns per gate: one thread per >= 64 K gates of fusion work
+    // Circuits in chunks of 16, in batch order: a slot whose gates carry the
+    // same angles (bit for bit) as in the previous circuit of the chunk copies
+    // that circuit's matrix -- a shift table changes one angle per circuit, so
+    // most slots skip the trig and the products.  One thread per >= 64 K gates.
     const int64_t gates = std::max<int64_t>(1, (int64_t)topo.kind.size());
-    parallel_for(C, std::max<int64_t>(8, 65536 / gates), [&](int64_t i) {
-        double* m = hmats.data() + (size_t)i * slots8;
-        circuit_matrices(plan, topo, angle_rows[i], m);
-        for (int sl = 0; sl < slots; ++sl) normalise_phase(m + (size_t)sl * 8);
+    const int64_t chunk = 16, nchunks = (C + chunk - 1) / chunk;
+    parallel_for(nchunks, std::max<int64_t>(1, 65536 / (gates * chunk)), [&](int64_t ch) {
+        for (int64_t i = ch * chunk; i < std::min(C, (ch + 1) * chunk); ++i) {
+            double* m = hmats.data() + (size_t)i * slots8;
+            const bool has_prev = i > ch * chunk;
+            for (int sl = 0; sl < slots; ++sl) {
+                bool same = has_prev;
+                if (same)
+                    for (int32_t ref : plan.ops[plan.mat_op[sl]].gates)
+                        if (ref >= 0 && std::memcmp(&angle_rows[i][ref], &angle_rows[i - 1][ref], sizeof(double))) {
+                            same = false;
+                            break;
+                        }
+                if (same) {
+                    std::memcpy(m + (size_t)sl * 8, m - slots8 + (size_t)sl * 8, 8 * sizeof(double));
+                } else {
+                    slot_matrix_with_pauli(plan, topo, angle_rows[i], sl, -1, m + (size_t)sl * 8);
+                    normalise_phase(m + (size_t)sl * 8);
+                }
+            }
+        }
     });
 
     // 2. deduplicate identical circuits (same topology + same matrices)
