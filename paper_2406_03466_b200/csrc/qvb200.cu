@@ -82,9 +82,9 @@ struct CachedPlan {
 
 
 // Hash of a matrix table, 8 bytes a step (candidates are confirmed with
-// memcmp, so only the spread matters; byte-wise FNV cost ~10 ms per 1 024
+// memcmp, so only the spread matters; a byte-wise FNV-1a cost ~10 ms per 1 024
 // circuits of 20q x 6L).
-uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
+uint64_t hash_words(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
     const unsigned char* p = static_cast<const unsigned char*>(data);
     size_t i = 0;
     for (; i + 8 <= bytes; i += 8) {
@@ -733,7 +733,7 @@ void GroupRun::run() {
         std::unordered_map<uint64_t, std::vector<int64_t>> seen;
         for (int64_t i = 0; i < C; ++i) {
             const double* row = hmats.data() + (size_t)i * slots8;
-            const uint64_t h = fnv1a(row, slots8 * sizeof(double));
+            const uint64_t h = hash_words(row, slots8 * sizeof(double));
             auto& cand = seen[h];
             int64_t u = -1;
             for (int64_t j : cand) {
@@ -971,7 +971,7 @@ void GroupRun::run() {
         std::vector<std::vector<uint64_t>> sig(U, std::vector<uint64_t>(P));
         for (int64_t u = 0; u < U; ++u)
             for (int p = 0; p < P; ++p)
-                sig[u][p] = fnv1a(umats.data() + (size_t)u * slots8 + (size_t)plan.pdesc[p].m0 * 8,
+                sig[u][p] = hash_words(umats.data() + (size_t)u * slots8 + (size_t)plan.pdesc[p].m0 * 8,
                                   (size_t)plan.pdesc[p].nm * 8 * sizeof(T), 0x9e3779b97f4a7c15ull + p);
         auto same_pass = [&](int64_t a, int64_t b, int p) {
             if (sig[a][p] != sig[b][p]) return false;
@@ -1206,7 +1206,8 @@ void GroupRun::run() {
         for (int64_t i = 0; i < C; ++i)
             std::memcpy(out + (size_t)circuits[i] * row, vals.data() + (size_t)uniq_of[i] * row, row * 8);
     } else if (R->kind == QV_OUT_JS && rows) {
-        std::vector<double> vals(C);
+        // an empty support leaves only the remainder term: (1 - 0)/2 ln 2
+        std::vector<double> vals(C, 0.5 * 0.69314718055994530942);
         if (ep.S > 0) d2h(E, vals.data(), d_jsrows, C * 8);
         for (int64_t i = 0; i < C; ++i) out[circuits[i]] = vals[i];
     } else if (R->kind == QV_OUT_JS) {
@@ -1250,6 +1251,24 @@ void execute(Engine& E, const qv_circuits* c, const qv_results* r, double* out, 
     validate(q);
     const int64_t need = output_size(c, r);
     if (need < 0 || out_len < need) throw ArgError("output buffer too small: need " + std::to_string(need));
+    if ((r->kind == QV_OUT_SUPPORT || r->kind == QV_OUT_JS) && r->support_count == 0) {
+        // An empty support: a JS loss is the remainder term alone, (1 - 0)/2 ln 2
+        // (ddcl.py:37-61 with no target entries); SUPPORT rows hold only the
+        // norm, taken from a run on the one-index support {0}.
+        if (r->kind == QV_OUT_JS) {
+            std::memset(E.stats, 0, sizeof(E.stats));
+            for (int64_t i = 0; i < c->n_circuits; ++i) out[i] = 0.5 * 0.69314718055994530942;
+            return;
+        }
+        const uint64_t zero = 0;
+        qv_results r1 = *r;
+        r1.support_count = 1;
+        r1.support = &zero;
+        std::vector<double> tmp((size_t)c->n_circuits * 2);
+        execute(E, c, &r1, tmp.data(), (int64_t)tmp.size());
+        for (int64_t i = 0; i < c->n_circuits; ++i) out[i] = tmp[2 * i + 1];
+        return;
+    }
     CK(cudaSetDevice(E.device));
     std::memset(E.stats, 0, sizeof(E.stats));
     E.t_entry = std::chrono::steady_clock::now();
@@ -1507,6 +1526,19 @@ void shift_js(Engine& E, const qv_circuits* c, int64_t nshift, const int64_t* ga
     if (nshift < 1) throw ArgError("no gates to shift");
     Request q{c, r, c->n_qubits, 1};
     validate(q);
+    if (r->support_count == 0) {
+        // an empty support: run on {0} with target 0 -- each loss is then the
+        // remainder term (1 - 0)/2 ln 2 up to rounding, and the shifted gates
+        // are still checked
+        const uint64_t zero = 0;
+        const double p0 = 0.0;
+        qv_results r1 = *r;
+        r1.support_count = 1;
+        r1.support = &zero;
+        r1.target = &p0;
+        shift_js(E, c, nshift, gates, &r1, out);
+        return;
+    }
     CK(cudaSetDevice(E.device));
     std::memset(E.stats, 0, sizeof(E.stats));
     E.t_entry = std::chrono::steady_clock::now();

@@ -283,6 +283,15 @@ def test_js_losses_against_own_targets(gpu, n):
     assert got[0] != got[-1]   # same state, different targets
     with pytest.raises(ValueError):
         backend.js_losses_targets(circuits, n, keys, rows[:-1])
+    # empty support: only the remainder term (1 - 0)/2 ln 2, as without rows
+    empty = backend.js_losses_targets(circuits[:2], n, [], np.zeros((2, 0)))
+    assert np.array_equal(empty, np.full(2, 0.5 * math.log(2.0)))
+    assert np.array_equal(backend.js_losses(circuits[:2], n, {}), empty)
+    norms = backend.support_probabilities(circuits[:2], n, [])
+    assert norms.shape == (2, 0)
+    if n > backend.tile_qubits():
+        pair = backend.shift_js_losses(qv.ddcl_circuit_template(n, layers), specs[0].theta, {}, [0, 5])
+        assert np.max(np.abs(pair - 0.5 * math.log(2.0))) < 1e-15
 
 
 @pytest.mark.parametrize("seed", range(8))
