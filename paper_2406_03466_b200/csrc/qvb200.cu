@@ -117,7 +117,7 @@ struct Engine {
     DevBuf<LaunchEntry> d_entries;
     DevBuf<double> d_partial;
     DevBuf<double2> d_partial2;
-    DevBuf<double> d_sup_out, d_js_out, d_full_out, d_pauli_out, d_target, d_delta;
+    DevBuf<double> d_sup_out, d_js_out, d_full_out, d_pauli_out, d_target, d_delta, d_cstage;
     DevBuf<uint64_t> d_support, d_tflip, d_tphase;
     DevBuf<int64_t> d_term_off, d_slots;
     DevBuf<int32_t> d_sup_off, d_sup_local, d_sup_pos, d_tsweep;
@@ -399,18 +399,23 @@ bool tma_pwg(int precision) {
 }
 // QVB200_TMA_ALT=1: the two teams take turns on the FP64 pipe (producer
 // -- measured).
+bool tma_cmats() {
+    static const bool c = !(getenv("QVB200_TMA_CMATS") && std::string(getenv("QVB200_TMA_CMATS")) == "0");
+    return c;
+}
 bool tma_alt() {
     static const bool a = getenv("QVB200_TMA_ALT") && std::string(getenv("QVB200_TMA_ALT")) == "1";
     return a;
 }
 template <typename T>
-TmaFn tma_kernel(int teams, bool direct, bool pwg, bool alt) {
+TmaFn tma_kernel(int teams, bool direct, bool pwg, bool alt, bool cm = false) {
     constexpr int ST = tma_stages<T>();
     constexpr int TBI = multi_tile_tb<T>();
     if constexpr (TBI != 8) {   // 8 K-amplitude tiles: one 512-thread team + the producer warp, or two
                                 // 256-thread teams holding two register groups per thread
         if (teams == 1) return &tma_pass_kernel<T, TBI, ST, 1, false, false, false>;
-        return &tma_pass_kernel<T, TBI, ST, 2, false, false, false>;
+        return cm ? &tma_pass_kernel<T, TBI, ST, 2, false, false, false, true>
+                  : &tma_pass_kernel<T, TBI, ST, 2, false, false, false>;
     } else {
         if (teams == 1) return &tma_pass_kernel<T, 8, ST, 1, false, false, false>;
         if (direct)
@@ -432,8 +437,9 @@ void set_kernel_attributes() {
         for (bool direct : {false, true})
             for (bool pwg : {false, true})
                 for (bool alt : {false, true})
-                    CK(cudaFuncSetAttribute(tma_kernel<T>(teams, direct, pwg, alt),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemCap));
+                    for (bool cm : {false, true})
+                        CK(cudaFuncSetAttribute(tma_kernel<T>(teams, direct, pwg, alt, cm),
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemCap));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -587,8 +593,20 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
             ta.trace = d_trace;
         }
 #endif
+        // complex64 two-team launches read their matrices from constant
+        // memory when the launch's tables fit (QVB200_TMA_CMATS=0 disables)
+        const bool cm = multi_tile_tb<T>() != 8 && teams == 2 && tma_cmats() &&
+                        (size_t)nstates * mat_bytes <= (size_t)kTmaConstBytes;
+        if (cm) {
+            V* stage = reinterpret_cast<V*>(E.d_cstage.get(kTmaConstBytes / sizeof(double)));
+            gather_cmats_kernel<V><<<(unsigned)nstates, 64, 0, E.stream>>>(d_ent, pd.m0, pd.nm, stage);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyToSymbolAsync(c_tma_mats, stage, (size_t)nstates * mat_bytes, 0, cudaMemcpyDeviceToDevice,
+                                       E.stream));
+            E.stats[0] += 1;
+        }
         CK(cudaEventRecord(e0, E.stream));
-        tma_kernel<T>(teams, direct, pwg, alt)<<<(unsigned)blocks, tma_threads(teams, pwg, multi_tile_tb<T>()), tma_smem, E.stream>>>(
+        tma_kernel<T>(teams, direct, pwg, alt, cm)<<<(unsigned)blocks, tma_threads(teams, pwg, multi_tile_tb<T>()), tma_smem, E.stream>>>(
             tmap, pd, ta, d_groups, d_ent, nstates, ntiles);
         CK(cudaGetLastError());
 #ifdef QV_TMA_TRACE
@@ -1622,7 +1640,7 @@ int qv_destroy(qv_handle h) {
         if (E->stream) cudaStreamSynchronize(E->stream);
         E->d_states.release(); E->d_mats.release(); E->d_entries.release(); E->d_partial.release();
         E->d_partial2.release(); E->d_sup_out.release(); E->d_js_out.release(); E->d_full_out.release();
-        E->d_pauli_out.release(); E->d_target.release(); E->d_support.release(); E->d_tflip.release();
+        E->d_pauli_out.release(); E->d_target.release(); E->d_cstage.release(); E->d_support.release(); E->d_tflip.release();
         E->d_tphase.release(); E->d_term_off.release(); E->d_slots.release(); E->d_sup_off.release();
         E->d_delta.release();
         E->d_sup_local.release(); E->d_sup_pos.release(); E->d_tsweep.release(); E->d_tfslot.release();
