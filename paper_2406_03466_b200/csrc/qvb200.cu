@@ -259,6 +259,8 @@ void validate(const Request& q) {
     }
     const qv_results* r = q.r;
     if (r->kind < QV_OUT_PAULI || r->kind > QV_OUT_COUNTS) throw ArgError("unknown result kind");
+    if (r->flags & ~QV_RES_TARGET_ROWS) throw ArgError("unknown result flags");
+    if ((r->flags & QV_RES_TARGET_ROWS) && r->kind != QV_OUT_JS) throw ArgError("target rows are a JS option");
     const uint64_t full = n >= 64 ? ~0ull : ((1ull << n) - 1);
     if (r->kind == QV_OUT_PAULI) {
         if (!r->term_offsets || !r->xmask || !r->ymask || !r->zmask) throw ArgError("null Pauli arrays");
@@ -272,10 +274,8 @@ void validate(const Request& q) {
             }
         }
     } else if (r->kind == QV_OUT_SUPPORT || r->kind == QV_OUT_JS) {
-        if (r->flags & ~QV_RES_TARGET_ROWS) throw ArgError("unknown result flags");
         if (r->support_count < 0 || (r->support_count > 0 && !r->support)) throw ArgError("bad support");
         if (r->kind == QV_OUT_JS && r->support_count > 0 && !r->target) throw ArgError("JS needs target probabilities");
-        if ((r->flags & QV_RES_TARGET_ROWS) && r->kind != QV_OUT_JS) throw ArgError("target rows are a JS option");
         for (int64_t s = 0; s < r->support_count; ++s) {
             if (r->support[s] & ~full) throw ArgError("support index beyond the register");
             if (s && r->support[s] <= r->support[s - 1]) throw ArgError("support must be sorted and unique");
@@ -1541,6 +1541,7 @@ void shift_js(Engine& E, const qv_circuits* c, int64_t nshift, const int64_t* ga
     if (!c || !gates || !r || !out) throw ArgError("null argument");
     if (c->n_circuits != 1) throw ArgError("shift pairs take exactly one base circuit");
     if (r->kind != QV_OUT_JS) throw ArgError("shift pairs return JS losses (results->kind = QV_OUT_JS)");
+    if (r->flags) throw ArgError("shift pairs take one target (no result flags)");
     if (nshift < 1) throw ArgError("no gates to shift");
     Request q{c, r, c->n_qubits, 1};
     validate(q);

@@ -283,6 +283,13 @@ def test_js_losses_against_own_targets(gpu, n):
     assert got[0] != got[-1]   # same state, different targets
     with pytest.raises(ValueError):
         backend.js_losses_targets(circuits, n, keys, rows[:-1])
+    # target rows are a JS-only option; unknown flags are rejected
+    from paper_2406_03466_b200 import native
+    from paper_2406_03466_b200.backend import lower_batch
+    sup = np.asarray([0, 1], np.uint64)
+    for kind, flags in ((native.QV_OUT_SUPPORT, native.QV_RES_TARGET_ROWS), (native.QV_OUT_JS, 6)):
+        with pytest.raises(native.NativeError):
+            backend._engine.execute(n, lower_batch(circuits[:1]), kind, support=sup, target=np.zeros(2), flags=flags)
     # empty support: only the remainder term (1 - 0)/2 ln 2, as without rows
     empty = backend.js_losses_targets(circuits[:2], n, [], np.zeros((2, 0)))
     assert np.array_equal(empty, np.full(2, 0.5 * math.log(2.0)))
