@@ -2,7 +2,7 @@
 native executor, host wall ms of the whole call, host ms before its first
 kernel, device ms, and the Python time around it.
 
-    python tools/host_overhead.py qcl4|mcvqe8|qcl20fwd [reps]
+    python tools/host_overhead.py qcl4|qcl20|mcvqe8|qcl20fwd [reps]
 """
 
 import json
@@ -25,6 +25,10 @@ def main():
     eng = native.engine(0, "complex128")
     if what == "qcl4":
         spec = qv.DdclSpec(4, 2, qv.random_angles(qv.ddcl_parameter_count(4, 2), 1), qv.random_target_distribution(4, 2))
+        run = lambda: qv.ddcl_gradient(spec, qv.VqpuPoolConfig(n_virtual_qpus=1))  # noqa: E731
+    elif what == "qcl20":
+        spec = qv.DdclSpec(20, 6, qv.random_angles(qv.ddcl_parameter_count(20, 6), 1),
+                           qv.random_target_distribution(20, 2))
         run = lambda: qv.ddcl_gradient(spec, qv.VqpuPoolConfig(n_virtual_qpus=1))  # noqa: E731
     elif what == "mcvqe8":
         ham = qv.aiem_hamiltonian(qv.random_aiem_coefficients(8, 0))
