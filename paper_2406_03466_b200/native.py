@@ -17,7 +17,8 @@ import numpy as np
 import os
 
 # QVB200_LIB selects an alternative build (e.g. the clock64-traced debug
-# library used by tools/trace_pass.py); the default is the product library.
+# library used by tools/tma_trace.py, or the diagnostic builds of
+# build.build_variant); the default is the product library.
 LIB_PATH = Path(os.environ.get("QVB200_LIB") or Path(__file__).resolve().parent / "libqvb200.so")
 
 QV_OK, QV_ERR_ARGUMENT, QV_ERR_CIRCUIT, QV_ERR_CUDA, QV_ERR_INTERNAL = range(5)
