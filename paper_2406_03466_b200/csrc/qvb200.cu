@@ -595,14 +595,17 @@ void launch_pass(Engine& E, const PassDesc& pd, const GroupDesc* d_groups, const
 #endif
         // complex64 two-team launches read their matrices from constant
         // memory when the launch's tables fit (QVB200_TMA_CMATS=0 disables)
-        const bool cm = multi_tile_tb<T>() != 8 && teams == 2 && tma_cmats() &&
-                        (size_t)nstates * mat_bytes <= (size_t)kTmaConstBytes;
+        const size_t cm_bytes = (size_t)nstates * pd.nm * (QV_TMA_PACKED ? kPackedMatBytes : 4 * sizeof(V));
+        const bool cm = multi_tile_tb<T>() != 8 && teams == 2 && tma_cmats() && cm_bytes <= (size_t)kTmaConstBytes;
         if (cm) {
             V* stage = reinterpret_cast<V*>(E.d_cstage.get(kTmaConstBytes / sizeof(double)));
-            gather_cmats_kernel<V><<<(unsigned)nstates, 64, 0, E.stream>>>(d_ent, pd.m0, pd.nm, stage);
+            if (QV_TMA_PACKED)
+                gather_cmats_packed_kernel<<<(unsigned)nstates, 64, 0, E.stream>>>(d_ent, pd.m0, pd.nm,
+                                                                                 reinterpret_cast<float2*>(stage));
+            else
+                gather_cmats_kernel<V><<<(unsigned)nstates, 64, 0, E.stream>>>(d_ent, pd.m0, pd.nm, stage);
             CK(cudaGetLastError());
-            CK(cudaMemcpyToSymbolAsync(c_tma_mats, stage, (size_t)nstates * mat_bytes, 0, cudaMemcpyDeviceToDevice,
-                                       E.stream));
+            CK(cudaMemcpyToSymbolAsync(c_tma_mats, stage, cm_bytes, 0, cudaMemcpyDeviceToDevice, E.stream));
             E.stats[0] += 1;
         }
         CK(cudaEventRecord(e0, E.stream));

@@ -227,11 +227,63 @@ __device__ __forceinline__ void team_sync(int team) {
 // broadcast shared loads -- 32q x 4L complex64 4.67 -> 4.55 s (same box);
 // for complex128 the eight LDC.64 per matrix cost more than they save.
 constexpr int kTmaConstBytes = 65536;
+#ifndef QV_TMA_PACKED
+#define QV_TMA_PACKED 1
+#endif
 __constant__ uint4 c_tma_mats[kTmaConstBytes / 16];
 template <typename V>
 __global__ void gather_cmats_kernel(const LaunchEntry* __restrict__ ent, int m0, int nm, V* __restrict__ out) {
     const V* src = reinterpret_cast<const V*>(ent[blockIdx.x].mats) + (size_t)m0 * 4;
     for (int q = threadIdx.x; q < nm * 4; q += blockDim.x) out[(size_t)blockIdx.x * nm * 4 + q] = src[q];
+}
+// complex64: each matrix as the seven packed FFMA2 operand pairs (+1 pad),
+// (m00.x, m00.x), (m01.x, m01.x), (-m01.y, m01.y), (m10.x, m10.x),
+// (-m10.y, m10.y), (m11.x, m11.x), (-m11.y, m11.y) -- 64 B per matrix
+constexpr int kPackedMatBytes = 64;
+__global__ void gather_cmats_packed_kernel(const LaunchEntry* __restrict__ ent, int m0, int nm, float2* __restrict__ out) {
+    const float2* src = reinterpret_cast<const float2*>(ent[blockIdx.x].mats) + (size_t)m0 * 4;
+    for (int q = threadIdx.x; q < nm; q += blockDim.x) {
+        const float2 a = src[4 * q], b = src[4 * q + 1], c = src[4 * q + 2], d = src[4 * q + 3];
+        float2* o = out + ((size_t)blockIdx.x * nm + q) * 8;
+        o[0] = make_float2(a.x, a.x);
+        o[1] = make_float2(b.x, b.x);
+        o[2] = make_float2(-b.y, b.y);
+        o[3] = make_float2(c.x, c.x);
+        o[4] = make_float2(-c.y, c.y);
+        o[5] = make_float2(d.x, d.x);
+        o[6] = make_float2(-d.y, d.y);
+        o[7] = make_float2(0.f, 0.f);
+    }
+}
+typedef unsigned long long f2p;
+__device__ __forceinline__ f2p f2_fma(f2p a, f2p b, f2p c) {
+    f2p d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2p f2_mul(f2p a, f2p b) {
+    f2p d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2p f2_swap(f2p a) {
+    f2p d;
+    asm("{\n\t.reg .f32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tmov.b64 %0, {hi, lo};\n\t}" : "=l"(d) : "l"(a));
+    return d;
+}
+// rot2 on packed (x, y) lanes: lane by lane the scalar rot2's FMA sequence
+__device__ __forceinline__ void rot2_packed(const f2p* M, float2& u2, float2& v2) {
+    f2p u = *reinterpret_cast<const f2p*>(&u2), v = *reinterpret_cast<const f2p*>(&v2);
+    const f2p us = f2_swap(u), vs = f2_swap(v);
+    f2p a = f2_mul(M[2], vs);
+    a = f2_fma(M[1], v, a);
+    a = f2_fma(M[0], u, a);
+    f2p b = f2_mul(M[6], vs);
+    b = f2_fma(M[5], v, b);
+    b = f2_fma(M[4], us, b);
+    b = f2_fma(M[3], u, b);
+    *reinterpret_cast<f2p*>(&u2) = a;
+    *reinterpret_cast<f2p*>(&v2) = b;
 }
 
 template <typename T, int TBITS, int STAGES, int TEAMS, bool DIRECT, bool PWG, bool ALT, bool CM = false>
@@ -241,7 +293,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
     static_assert(!DIRECT || TEAMS > 1, "direct stores are issued by the teams themselves");
     static_assert(!PWG || (TEAMS == 2 && !DIRECT), "the producer warpgroup serves two teams with bulk stores");
     static_assert(!ALT || TEAMS == 2, "alternating math needs two teams");
-    constexpr bool PRODUCER_THREAD = TEAMS == 1 || PWG;   // a thread outside the teams stores and reloads stages
+    constexpr bool PRODUCER_THREAD = TEAMS == 1 || PWG;
+    constexpr bool PACKED = CM && sizeof(T) == 4 && QV_TMA_PACKED;   // complex64 FFMA2 from packed constant operands   // a thread outside the teams stores and reloads stages
     typedef typename Cx<T>::V V;
     constexpr int R = reg_bits(sizeof(T) == 8 ? 0 : 1);
     constexpr int NA = 1 << R;
@@ -439,6 +492,8 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
         const uint32_t boff = s * TILE;   // a multiple of 2^15 >= every slot offset
         const V* smat = CM ? reinterpret_cast<const V*>(c_tma_mats) + (size_t)(((int)blockIdx.x + i * G) % nstates) * pd.nm * 4
                            : reinterpret_cast<const V*>(smem_raw + STAGES * TILE + s * kTmaMatBytes);
+        const f2p* cpk = reinterpret_cast<const f2p*>(c_tma_mats) + (size_t)(((int)blockIdx.x + i * G) % nstates) * pd.nm * 8;
+        (void)cpk;
         V* __restrict__ out = nullptr;
         if constexpr (DIRECT) {
             // the stage is released before the last group's math: its
@@ -454,7 +509,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
             const GroupDesc& GD = sg[g];
             const int4 mats = *reinterpret_cast<const int4*>(GD.mat);
             V m00, m01, m10, m11;
-            if (mats.x >= 0) {
+            if (!PACKED && mats.x >= 0) {
                 const V* M = smat + mats.x * 4;
                 m00 = M[0]; m01 = M[1]; m10 = M[2]; m11 = M[3];
             }
@@ -513,6 +568,24 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                 if (team == 0 && phase >= 1 && phase <= phases1) mbar_wait(tok0, (uint32_t)((phase - 1) & 1));
                 if (team == 1 && phase < phases0) mbar_wait(tok0 + 8, (uint32_t)(phase & 1));
             }
+            if constexpr (PACKED) {
+                // complex64 + constant matrices: packed FFMA2 operands straight from LDC
+#pragma unroll
+                for (int r = 0; r < (QV_TMA_DIAG_NOMATH ? 0 : R); ++r) {
+                    const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
+                    if (mi >= 0) {
+                        const f2p* M = cpk + (size_t)mi * 8;
+                        f2p pm[7];
+#pragma unroll
+                        for (int e = 0; e < 7; ++e) pm[e] = M[e];
+#pragma unroll
+                        for (int h = 0; h < SUB; ++h)
+#pragma unroll
+                            for (int j = 0; j < NA; ++j)
+                                if (!((j >> r) & 1)) rot2_packed(pm, a[h][j], a[h][j | (1 << r)]);
+                    }
+                }
+            } else {
 #pragma unroll
             for (int r = 0; r < (QV_TMA_DIAG_NOMATH ? 0 : R); ++r) {
                 const int mi = r == 0 ? mats.x : r == 1 ? mats.y : r == 2 ? mats.z : mats.w;
@@ -527,6 +600,7 @@ tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassDesc pd, con
                         for (int j = 0; j < NA; ++j)
                             if (!((j >> r) & 1)) rot2<V>(m00, m01, m10, m11, a[h][j], a[h][j | (1 << r)]);
                 }
+            }
             }
             if constexpr (ALT) {   // hand the FP64 pipe to the other team
                 // one arrival per warp (256 arrivals on one word serialise)
